@@ -1,0 +1,323 @@
+/*
+ * oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU implementation of what the hot path of
+ * Dettmers, Lewis, Shleifer & Zettlemoyer, "8-bit Optimizers via Block-wise
+ * Quantization" (arXiv 2110.02861) computes.  Citations are to
+ * /root/reference/PAPER.md as "P:<line>" (section / equation in brackets) and to
+ * the readings "G<n>" listed in DESIGN.md section 3 (taken from SURVEY.md 8(c)).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+ * leg may load this file.  It shares no code, header, table or constant
+ * generator with the CUDA library under paper_2110_02861_b200/; neither side
+ * includes or links the other.
+ *
+ * Compiled with  gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math  so that every
+ * float expression written below is one IEEE-754 binary32 round-to-nearest-even
+ * operation per operator (no FMA contraction, no reassociation).
+ *
+ * Parity status of every exported function (pins live in tests/test_oracle_*.py):
+ *   oracle_dynamic_codebook   pinned: exact rational closed form, invariants,
+ *                              golden hashes (tests/golden/)
+ *   oracle_nearest_code        pinned: brute-force argmin (numpy) incl. exact ties
+ *   oracle_quantize_blockwise  pinned: SPEC worked examples, absmax = np.max|x|,
+ *                              half-gap bound, block independence
+ *   oracle_dequantize_blockwise pinned: Q[code]*N by numpy
+ *   oracle_optim32bit_step     pinned: torch.optim.{Adam,AdamW,SGD} (CPU fp32),
+ *                              hand arithmetic S:315/S:324, t=1 closed form
+ *   oracle_optim8bit_step      pinned: == 32-bit step + explicit block quantize
+ *                              (bit-exact), 8-bit vs 32-bit within quantization
+ *                              error over 10 steps
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORACLE_ADAM 0
+#define ORACLE_ADAMW 1
+#define ORACLE_MOMENTUM 2
+
+typedef struct {
+    double lr;            /* alpha,  Eq.1/Eq.2 */
+    double beta1;         /* beta_1 (Momentum: beta of Eq.1) */
+    double beta2;         /* beta_2, Adam only */
+    double eps;           /* epsilon, Adam only */
+    double weight_decay;  /* G10: AdamW decoupled, Adam/Momentum L2 */
+    int bias_correction;  /* G8 */
+} oracle_hparams;
+
+/* ------------------------------------------------------------------------- */
+/* 1. Dynamic (tree) quantization data type -- P:90 [S2.3], P:118 [S3.2], G1/G2 */
+/* ------------------------------------------------------------------------- */
+
+static int cmp_float_asc(const void* a, const void* b) {
+    float x = *(const float*)a, y = *(const float*)b;
+    return (x > y) - (x < y);
+}
+
+/*
+ * Decode one 8-bit pattern of the dynamic data type.
+ *
+ * "(1) The first bit of the data type is reserved for a sign. (2) The
+ * number of subsequent zero bits indicates the magnitude of the exponent. (3)
+ * The first bit that is set to one indicates that all following values are
+ * reserved for (4) linear quantization."  The exponent is a power of ten
+ * (base 10^0 = 1, each zero bit divides by 10, minimum 10^-7: P:400).
+ * P:118 (unsigned): the sign bit is re-purposed as a *fixed* extra fraction bit.
+ *
+ * Reading G1: with z leading zeros and F fraction bits holding integer f, the
+ * linear part quantizes the decade (0.1, 1] into 2^F equal bins and takes the
+ * bin midpoint:   magnitude = 10^-z * (0.1 + 0.9 * (f + 0.5) / 2^F).
+ * The two patterns without an indicator bit become 0 and +1.0 (G1).
+ * Evaluated in double, rounded once to binary32 (G2).
+ */
+static float decode_pattern(int is_signed, unsigned pattern) {
+    static const double decade[7] = {1.0, 0.1, 0.01, 1e-3, 1e-4, 1e-5, 1e-6};
+    unsigned lead = (pattern >> 7) & 1u;         /* sign bit (signed) or fixed fraction bit (unsigned) */
+    unsigned rest = pattern & 0x7fu;                                       /* 7 bits: zeros, indicator, fraction */
+    int z = 0;
+    while (z < 7 && ((rest >> (6 - z)) & 1u) == 0u) z++;
+    if (z == 7) {
+        /* no indicator bit: the two special patterns -> 0 and +1.0 (G1) */
+        return lead ? 1.0f : 0.0f;
+    }
+    int nfrac7 = 6 - z;                          /* fraction bits after the indicator */
+    unsigned f = rest & ((1u << nfrac7) - 1u);
+    int F = nfrac7;
+    if (!is_signed) {                            /* fixed bit = one more fraction bit */
+        f = (lead << nfrac7) | f;
+        F = nfrac7 + 1;
+    }
+    double L = (double)(1u << F);
+    double mag = decade[z] * (0.1 + 0.9 * ((double)f + 0.5) / L);
+    double v = (is_signed && lead) ? -mag : mag;
+    return (float)v;
+}
+
+/* Q^map as an ascending table of 256 binary32 values; codes are indices into it (G4). */
+int oracle_dynamic_codebook(int is_signed, float out[256]) {
+    for (unsigned p = 0; p < 256; p++) out[p] = decode_pattern(is_signed, p);
+    qsort(out, 256, sizeof(float), cmp_float_asc);
+    for (int i = 1; i < 256; i++)
+        if (!(out[i - 1] < out[i])) return -1;   /* must be 256 distinct values */
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* 2. Nearest code -- Eq.3: argmin_j |Q_j - T_i/N|, via binary search */
+/* ------------------------------------------------------------------------- */
+
+/*
+ * Returns argmin_{j in 0..255} |Q[j] - y| with ties broken toward the lower
+ * index (G6).  Q must be strictly ascending.  As Eq.3 says, the closest value
+ * is found "via a binary search": lower_bound finds the first Q[hi] >= y, and
+ * the answer is whichever of Q[hi-1], Q[hi] is closer.  The two distances are
+ * compared in double, where the difference of two binary32 numbers that
+ * bracket y is exact.
+ */
+int oracle_nearest_code(const float Q[256], float y) {
+    int lo = 0, hi = 256;                        /* lower_bound over Q */
+    while (lo < hi) {
+        int mid = (lo + hi) / 2;
+        if (Q[mid] < y) lo = mid + 1; else hi = mid;
+    }
+    if (hi == 0) return 0;
+    if (hi == 256) return 255;
+    double d_lo = fabs((double)y - (double)Q[hi - 1]);
+    double d_hi = fabs((double)Q[hi] - (double)y);
+    return (d_hi < d_lo) ? hi : hi - 1;          /* tie -> lower index */
+}
+
+/* ------------------------------------------------------------------------- */
+/* 3. Block-wise quantization -- Eq.4, dequantization P:71          */
+/* ------------------------------------------------------------------------- */
+
+/* Number of blocks: ceil(n / B); the last block may be short (G5). */
+static int64_t num_blocks(int64_t n, int64_t B) { return (n + B - 1) / B; }
+
+/* N_b = max(|T_b|) */
+static float block_absmax(const float* x, int64_t len) {
+    float N = 0.0f;
+    for (int64_t i = 0; i < len; i++) {
+        float a = fabsf(x[i]);
+        if (a > N) N = a;
+    }
+    return N;
+}
+
+/* T^Q_bi = argmin_j |Q_j - T_bi / N_b|   (Eq.4).  N_b = 0 means the block is all
+ * zeros; its normalized values are taken as 0 (G7). */
+static void quantize_block(const float Q[256], const float* x, int64_t len, float* absmax, uint8_t* codes) {
+    float N = block_absmax(x, len);
+    *absmax = N;
+    for (int64_t i = 0; i < len; i++) {
+        float y = (N > 0.0f) ? x[i] / N : 0.0f;
+        codes[i] = (uint8_t)oracle_nearest_code(Q, y);
+    }
+}
+
+int oracle_quantize_blockwise(const float Q[256], const float* x, int64_t n, int64_t B,
+                              float* absmax, uint8_t* codes) {
+    if (n < 0 || B < 1) return -1;
+    for (int64_t b = 0; b < num_blocks(n, B); b++) {
+        int64_t start = b * B, len = (n - start < B) ? n - start : B;
+        quantize_block(Q, x + start, len, absmax + b, codes + start);
+    }
+    return 0;
+}
+
+/* T^D_i = Q^map(T^Q_i) * N, with N = N_b of the element's block. */
+int oracle_dequantize_blockwise(const float Q[256], const uint8_t* codes, const float* absmax,
+                                int64_t n, int64_t B, float* out) {
+    if (n < 0 || B < 1) return -1;
+    for (int64_t i = 0; i < n; i++) out[i] = Q[codes[i]] * absmax[i / B];
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* 4. Optimizer updates in 32-bit -- Eq.1, Eq.2              */
+/* ------------------------------------------------------------------------- */
+
+typedef struct {
+    int kind;
+    float lr, beta1, beta2, one_minus_beta1, one_minus_beta2;
+    float step_size, eps_hat, weight_decay, decay;
+} scalars;
+
+/*
+ * Host scalars, computed in double and rounded once to binary32 (G8-G10).
+ * Bias correction (G8) uses Kingma & Ba's folded form (Adam paper, S2 last
+ * paragraph):  alpha_t = alpha*sqrt(1-beta2^t)/(1-beta1^t),
+ * eps_hat = eps*sqrt(1-beta2^t); then w -= alpha_t * m/(sqrt(r) + eps_hat).
+ */
+static scalars make_scalars(int kind, const oracle_hparams* hp, int64_t step) {
+    scalars s;
+    s.kind = kind;
+    s.lr = (float)hp->lr;
+    s.beta1 = (float)hp->beta1;
+    s.beta2 = (float)hp->beta2;
+    s.one_minus_beta1 = (float)(1.0 - hp->beta1);
+    s.one_minus_beta2 = (float)(1.0 - hp->beta2);
+    if (hp->bias_correction) {
+        double bc1 = 1.0 - pow(hp->beta1, (double)step);
+        double bc2 = 1.0 - pow(hp->beta2, (double)step);
+        s.step_size = (float)(hp->lr * sqrt(bc2) / bc1);
+        s.eps_hat = (float)(hp->eps * sqrt(bc2));
+    } else {
+        s.step_size = (float)hp->lr;
+        s.eps_hat = (float)hp->eps;
+    }
+    s.weight_decay = (float)hp->weight_decay;
+    s.decay = (float)(1.0 - hp->lr * hp->weight_decay);
+    return s;
+}
+
+/*
+ * One element of the 32-bit update, in the order Eq.1/Eq.2 write it; every
+ * operator is one binary32 rounding (G9).  Weight decay (G10): AdamW scales w
+ * by (1 - lr*wd) first (decoupled, Loshchilov & Hutter, cited P:134);
+ * Adam and Momentum add wd*w to the gradient (L2) when wd != 0.
+ */
+static void update_element(const scalars* s, float* w, float g, float* m, float* r) {
+    if (s->kind == ORACLE_ADAMW) {
+        *w = *w * s->decay;
+    } else if (s->weight_decay != 0.0f) {
+        g = g + s->weight_decay * *w;
+    }
+    if (s->kind == ORACLE_MOMENTUM) {
+        /* Eq.1: m_t = beta1*m_{t-1} + g_t ;  w_t = w_{t-1} - alpha*m_t.
+         * m_0 = g_0 follows from the zero initial state. */
+        *m = s->beta1 * *m + g;
+        *w = *w - s->lr * *m;
+    } else {
+        /* Eq.2: m_t = beta1*m + (1-beta1)*g ;  r_t = beta2*r + (1-beta2)*g^2 ;
+         *       w_t = w - alpha*m_t/(sqrt(r_t)+eps)   (alpha, eps -> step_size, eps_hat) */
+        *m = s->beta1 * *m + s->one_minus_beta1 * g;
+        *r = s->beta2 * *r + s->one_minus_beta2 * (g * g);
+        *w = *w - s->step_size * (*m / (sqrtf(*r) + s->eps_hat));
+    }
+}
+
+/* 32-bit optimizer step (states m, r in fp32; r unused for Momentum). */
+int oracle_optim32bit_step(int kind, float* p, const float* g, float* m, float* r, int64_t n,
+                           const oracle_hparams* hp, int64_t step) {
+    if (kind < 0 || kind > 2 || n < 0 || step < 1) return -1;
+    scalars s = make_scalars(kind, hp, step);
+    float dummy = 0.0f;
+    for (int64_t i = 0; i < n; i++)
+        update_element(&s, &p[i], g[i], &m[i], kind == ORACLE_MOMENTUM ? &dummy : &r[i]);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* 5. 8-bit optimizer step -- S3, Fig.1 caption                */
+/*    dequantize -> 32-bit update (Eq.1/2) -> block absmax        */
+/*    -> requantize (Eq.4); w uses the 32-bit post-update states (G12).          */
+/*    s1 uses the signed data type, s2 (strictly positive) the unsigned (G14).  */
+/* ------------------------------------------------------------------------- */
+
+typedef struct {
+    int kind;
+    float* p;
+    const float* g;
+    uint8_t* s1;
+    uint8_t* s2;
+    float* absmax1;
+    float* absmax2;
+    int64_t n, B, b_begin, b_end;
+    const scalars* s;
+    const float* Qs;
+    const float* Qu;
+} step_job;
+
+static void* step_blocks(void* arg) {
+    step_job* j = (step_job*)arg;
+    float* m = (float*)malloc(sizeof(float) * (size_t)j->B);
+    float* r = (float*)malloc(sizeof(float) * (size_t)j->B);
+    for (int64_t b = j->b_begin; b < j->b_end; b++) {
+        int64_t start = b * j->B, len = (j->n - start < j->B) ? j->n - start : j->B;
+        /* dequantize: T^D = Q^map(T^Q) * N_b */
+        for (int64_t i = 0; i < len; i++) {
+            m[i] = j->Qs[j->s1[start + i]] * j->absmax1[b];
+            r[i] = (j->kind == ORACLE_MOMENTUM) ? 0.0f : j->Qu[j->s2[start + i]] * j->absmax2[b];
+        }
+        /* 32-bit update, element by element */
+        for (int64_t i = 0; i < len; i++) update_element(j->s, &j->p[start + i], j->g[start + i], &m[i], &r[i]);
+        /* block-wise requantization of the new states (Eq.4) */
+        quantize_block(j->Qs, m, len, &j->absmax1[b], j->s1 + start);
+        if (j->kind != ORACLE_MOMENTUM) quantize_block(j->Qu, r, len, &j->absmax2[b], j->s2 + start);
+    }
+    free(m);
+    free(r);
+    return NULL;
+}
+
+/*
+ * g is binary32 (16-bit gradients are widened exactly by the caller, G13).
+ * Blocks are independent, so nthreads > 1 splits the block range into
+ * contiguous pieces; results do not depend on nthreads.
+ */
+int oracle_optim8bit_step(int kind, float* p, const float* g, uint8_t* s1, uint8_t* s2, float* absmax1,
+                          float* absmax2, int64_t n, int64_t B, const oracle_hparams* hp, int64_t step,
+                          int nthreads) {
+    if (kind < 0 || kind > 2 || n < 0 || B < 1 || step < 1) return -1;
+    float Qs[256], Qu[256];
+    if (oracle_dynamic_codebook(1, Qs) != 0 || oracle_dynamic_codebook(0, Qu) != 0) return -1;
+    scalars s = make_scalars(kind, hp, step);
+    int64_t nb = num_blocks(n, B);
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    step_job jobs[256];
+    for (int t = 0; t < nthreads; t++) {
+        step_job j = {kind, p, g, s1, s2, absmax1, absmax2, n, B, nb * t / nthreads, nb * (t + 1) / nthreads,
+                      &s, Qs, Qu};
+        jobs[t] = j;
+    }
+    for (int t = 1; t < nthreads; t++) pthread_create(&th[t], NULL, step_blocks, &jobs[t]);
+    step_blocks(&jobs[0]);
+    for (int t = 1; t < nthreads; t++) pthread_join(th[t], NULL);
+    return 0;
+}
