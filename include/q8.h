@@ -1,0 +1,141 @@
+/*
+ * q8.h -- C ABI of the B200-native (sm_100a) block-wise dynamic 8-bit optimizer step.
+ *
+ * Method: Dettmers, Lewis, Shleifer & Zettlemoyer, "8-bit Optimizers via Block-wise
+ * Quantization" (arXiv 2110.02861).  "P:<line>" cites /root/reference/PAPER.md;
+ * "G<n>" cites the readings in DESIGN.md section 3.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Plain C: pointers, sizes, enums; no torch types.  Link: libq8.so (cudart static).
+ *  - "_dev" pointers are CUDA device pointers on the current device; "_host" pointers
+ *    are host memory.  The CALLER owns every buffer; the library never allocates on
+ *    the hot path.  It owns only immutable internal tables (the two dynamic codebooks
+ *    and their search tables), created once per device on first use.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Work is
+ *    enqueued asynchronously; argument validation is synchronous.  Asynchronous CUDA
+ *    errors surface at the caller's next synchronisation (CUDA convention).
+ *  - Codes are uint8 indices into the ASCENDING 256-entry codebook (G4); block b of a
+ *    tensor covers elements [b*B, min((b+1)*B, n)) and has one fp32 absmax N_b;
+ *    the last block may be short (G5).  Blocks never span tensors.
+ *  - Every call returns a q8_status; on failure q8_last_error() describes why
+ *    (thread-local string, valid until the next call on the same thread).
+ *  - n == 0 is a valid no-op (empty shards under ZeRO padding are normal).
+ *  - Thread-safe and re-entrant: the library holds no mutable state besides its
+ *    per-device table cache (guarded by a mutex).
+ */
+#ifndef Q8_H
+#define Q8_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    Q8_OK = 0,
+    Q8_ERR_INVALID = -1,      /* bad argument: NULL with n > 0, n < 0, misaligned, bad enum/hparam */
+    Q8_ERR_UNSUPPORTED = -2,  /* valid request this build does not implement (blocksize != 2048) */
+    Q8_ERR_CUDA = -3          /* a CUDA runtime call or kernel launch failed */
+} q8_status;
+
+typedef enum { Q8_F32 = 0, Q8_F16 = 1, Q8_BF16 = 2 } q8_dtype;          /* gradient dtype (G13) */
+typedef enum { Q8_ADAM = 0, Q8_ADAMW = 1, Q8_MOMENTUM = 2 } q8_kind;    /* Eq.2, AdamW, Eq.1 */
+
+/* Optimizer hyper-parameters (host struct, doubles; every derived fp32 scalar is computed
+ * in double and rounded once, G8-G10).
+ *   lr            alpha of Eq.1/Eq.2, >= 0
+ *   beta1         beta_1 of Eq.2; the momentum beta of Eq.1 for Q8_MOMENTUM; in [0, 1)
+ *   beta2         beta_2 of Eq.2, in [0, 1) (ignored by Q8_MOMENTUM)
+ *   eps           epsilon of Eq.2, > 0 (ignored by Q8_MOMENTUM)
+ *   weight_decay  >= 0.  Q8_ADAMW: decoupled, w *= (1 - lr*wd) before the update.
+ *                 Q8_ADAM / Q8_MOMENTUM: L2, g += wd*w (G10)
+ *   bias_correction  0/1: Kingma & Ba's folded correction alpha_t, eps_hat (G8);
+ *                 ignored by Q8_MOMENTUM */
+typedef struct {
+    double lr, beta1, beta2, eps, weight_decay;
+    int32_t bias_correction;
+} q8_hparams;
+
+/* One tensor of a multi-tensor step (all device pointers; s2/absmax2 may be NULL for
+ * Q8_MOMENTUM).  Alignment: p 16 B, g 16 B (fp32) / 8 B (16-bit), s1/s2 4 B. */
+typedef struct {
+    float* p;
+    const void* g;
+    uint8_t* s1;
+    uint8_t* s2;
+    float* absmax1;
+    float* absmax2;
+    int64_t n;
+} q8_tensor;
+
+/* Fill out_host[256] with the dynamic data type's 256 values in ascending order.
+ * is_signed = 1: dynamic tree quantization (S2.3): sign, run of zero bits =
+ *                decade exponent, indicator bit, linear fraction; used for state 1.
+ * is_signed = 0: dynamic quantization (S3.2): the sign bit re-purposed as a fixed
+ *                extra fraction bit; used for the strictly positive state 2.
+ * Reading G1/G2: bin-midpoint linear fraction, specials {0, +1}, built in double and
+ * rounded once to fp32.  Pure host function.  Errors: INVALID if out_host is NULL. */
+q8_status q8_create_dynamic_codebook(int32_t is_signed, float* out_host);
+
+/* Block-wise quantization, Eq.4:
+ *   N_b = max_i |x_i| over block b;  y_i = x_i / N_b (IEEE fp32 division; y = 0
+ *   when N_b = 0, G7);  codes_i = argmin_j |code_dev[j] - y_i|, ties to the lower index (G6).
+ *   x_dev      [n] fp32, 16-B aligned (read)
+ *   code_dev   [256] fp32 device table, strictly ascending (read; e.g. a table made by
+ *              q8_create_dynamic_codebook and copied to the device)
+ *   absmax_dev [ceil(n/B)] fp32 (written)
+ *   codes_dev  [n] uint8, 4-B aligned (written)
+ *   blocksize  must be 2048 (else UNSUPPORTED, G16). */
+q8_status q8_quantize_blockwise(const float* code_dev, const float* x_dev, float* absmax_dev,
+                                uint8_t* codes_dev, int64_t n, int32_t blocksize, void* stream);
+
+/* Block-wise dequantization: out_i = code_dev[codes_i] * absmax_dev[i / B] (one fp32
+ * multiply).  codes_dev [n] uint8 4-B aligned, absmax_dev [ceil(n/B)], out_dev [n] fp32 16-B
+ * aligned.  blocksize must be 2048. */
+q8_status q8_dequantize_blockwise(const float* code_dev, const uint8_t* codes_dev, const float* absmax_dev,
+                                  float* out_dev, int64_t n, int32_t blocksize, void* stream);
+
+/* The fused 8-bit optimizer step (S3; Fig.1), in place, for one tensor:
+ * for each block b:
+ *   1. dequantize  m = Q_s[s1_i] * absmax1[b],  r = Q_u[s2_i] * absmax2[b]
+ *   2. update in fp32, element by element in registers: Eq.2 (Q8_ADAM/ADAMW,
+ *      bias correction G8, weight decay G10) or Eq.1 (Q8_MOMENTUM); p uses the fp32
+ *      post-update states (G12)
+ *   3. absmax1[b] = max|m|, absmax2[b] = max|r| over the block
+ *   4. requantize s1 = nearest code of m/absmax1[b] in Q_s (signed), s2 likewise in
+ *      Q_u (unsigned) (Eq.4, G14)
+ * Arguments (device pointers unless noted):
+ *   p        [n] fp32 parameters, read-modify-write, 16-B aligned
+ *   g        [n] gradients of g_dtype (fp32 16-B aligned, fp16/bf16 8-B aligned), read
+ *   s1, s2   [n] uint8 codes (state 1 / state 2), RMW, 4-B aligned; s2 unused (may be
+ *            NULL) for Q8_MOMENTUM.  All-zero codes+absmax is the valid initial state.
+ *   absmax1, absmax2  [ceil(n/2048)] fp32, RMW; absmax2 unused for Q8_MOMENTUM
+ *   blocksize must be 2048; step = t >= 1, the 1-based index of this update (the caller
+ *   owns t, as torch's state['step']); hp host pointer.
+ * Buffers must not alias each other. */
+q8_status q8_optim8bit_step(q8_kind kind, float* p, const void* g, q8_dtype g_dtype, uint8_t* s1,
+                            uint8_t* s2, float* absmax1, float* absmax2, int64_t n, int32_t blocksize,
+                            const q8_hparams* hp, int64_t step, void* stream);
+
+/* Multi-tensor variant (one launch per up-to-Q8_MAX_TENSORS_PER_LAUNCH tensors): the same
+ * step applied to every tensor of tensors_host[num_tensors] (a HOST array of device-pointer
+ * descriptors, copied into the launch).  Blocks are per tensor: each tensor's last
+ * block may be short.  Tensors with n == 0 are skipped.  Same validation as above, per tensor. */
+#define Q8_MAX_TENSORS_PER_LAUNCH 384
+q8_status q8_optim8bit_step_multi(q8_kind kind, q8_dtype g_dtype, const q8_tensor* tensors_host,
+                                  int32_t num_tensors, int32_t blocksize, const q8_hparams* hp, int64_t step,
+                                  void* stream);
+
+/* Thread-local description of the last error ("" after success). */
+const char* q8_last_error(void);
+
+/* Library version string, e.g. "q8 0.1 sm_100a". */
+const char* q8_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* Q8_H */

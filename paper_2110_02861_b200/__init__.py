@@ -1,0 +1,16 @@
+"""B200-native (sm_100a) block-wise dynamic 8-bit optimizer step (Dettmers et al. 2021,
+arXiv 2110.02861).
+
+The hot path lives in ``csrc/`` (CUDA kernels behind the C ABI ``include/q8.h``, built
+into ``libq8.so``); this package is the thin Python binding plus the torch-facing
+optimizer classes and the ZeRO-1 sharding wrapper.  There is no CPU fallback.
+"""
+from ._binding import (BLOCKSIZE, MAX_TENSORS_PER_LAUNCH, Q8Error, TensorList, create_dynamic_codebook,
+                       dequantize_blockwise, hparams, nblocks, optim8bit_step, optim8bit_step_multi,
+                       quantize_blockwise, version)
+
+__all__ = [
+    "BLOCKSIZE", "MAX_TENSORS_PER_LAUNCH", "Q8Error", "TensorList", "create_dynamic_codebook",
+    "dequantize_blockwise", "hparams", "nblocks", "optim8bit_step", "optim8bit_step_multi", "quantize_blockwise",
+    "version",
+]

@@ -1,0 +1,186 @@
+"""Thin ctypes binding over libq8.so (include/q8.h).  Argument marshalling only: every step
+of the hot path runs in the CUDA kernels of csrc/.  There is no CPU fallback; if the
+library cannot be loaded, importing this module raises."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libq8.so")
+
+Q8_OK, Q8_ERR_INVALID, Q8_ERR_UNSUPPORTED, Q8_ERR_CUDA = 0, -1, -2, -3
+Q8_F32, Q8_F16, Q8_BF16 = 0, 1, 2
+Q8_ADAM, Q8_ADAMW, Q8_MOMENTUM = 0, 1, 2
+MAX_TENSORS_PER_LAUNCH = 384
+BLOCKSIZE = 2048
+
+KINDS = {"adam": Q8_ADAM, "adamw": Q8_ADAMW, "momentum": Q8_MOMENTUM}
+GDTYPES = {torch.float32: Q8_F32, torch.float16: Q8_F16, torch.bfloat16: Q8_BF16}
+
+EXPORTS = ("q8_create_dynamic_codebook", "q8_quantize_blockwise", "q8_dequantize_blockwise",
+           "q8_optim8bit_step", "q8_optim8bit_step_multi", "q8_last_error", "q8_version")
+
+
+class Q8Error(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"q8 status {status}: {msg}")
+        self.status = status
+
+
+class HParams(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
+                ("eps", ctypes.c_double), ("weight_decay", ctypes.c_double), ("bias_correction", ctypes.c_int32)]
+
+
+class TensorDesc(ctypes.Structure):
+    _fields_ = [("p", ctypes.c_void_p), ("g", ctypes.c_void_p), ("s1", ctypes.c_void_p), ("s2", ctypes.c_void_p),
+                ("absmax1", ctypes.c_void_p), ("absmax2", ctypes.c_void_p), ("n", ctypes.c_int64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    lib.q8_create_dynamic_codebook.argtypes = [i32, vp]
+    lib.q8_quantize_blockwise.argtypes = [vp, vp, vp, vp, i64, i32, vp]
+    lib.q8_dequantize_blockwise.argtypes = [vp, vp, vp, vp, i64, i32, vp]
+    lib.q8_optim8bit_step.argtypes = [i32, vp, vp, i32, vp, vp, vp, vp, i64, i32, ctypes.POINTER(HParams), i64, vp]
+    lib.q8_optim8bit_step_multi.argtypes = [i32, i32, ctypes.POINTER(TensorDesc), i32, i32,
+                                            ctypes.POINTER(HParams), i64, vp]
+    for f in EXPORTS[:-2]:
+        getattr(lib, f).restype = ctypes.c_int
+    lib.q8_last_error.restype = ctypes.c_char_p
+    lib.q8_version.restype = ctypes.c_char_p
+    return lib
+
+
+lib = _load()
+
+
+def _check(status: int):
+    if status != Q8_OK:
+        raise Q8Error(status, lib.q8_last_error().decode())
+
+
+def _stream(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _dev_ptr(t: torch.Tensor | None, dtype=None, name="tensor") -> int | None:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    return t.data_ptr()
+
+
+def version() -> str:
+    return lib.q8_version().decode()
+
+
+def nblocks(n: int, blocksize: int = BLOCKSIZE) -> int:
+    return (n + blocksize - 1) // blocksize
+
+
+def create_dynamic_codebook(signed: bool) -> torch.Tensor:
+    """Host call: the 256 ascending fp32 values of the (un)signed dynamic data type."""
+    out = torch.empty(256, dtype=torch.float32)
+    _check(lib.q8_create_dynamic_codebook(1 if signed else 0, out.data_ptr()))
+    return out
+
+
+def quantize_blockwise(code: torch.Tensor, x: torch.Tensor, absmax: torch.Tensor | None = None,
+                       codes: torch.Tensor | None = None, blocksize: int = BLOCKSIZE):
+    n = x.numel()
+    if absmax is None:
+        absmax = torch.empty(nblocks(n, blocksize), dtype=torch.float32, device=x.device)
+    if codes is None:
+        codes = torch.empty(n, dtype=torch.uint8, device=x.device)
+    if codes.numel() != n or absmax.numel() < nblocks(n, blocksize) or code.numel() != 256:
+        raise ValueError("size mismatch")
+    _check(lib.q8_quantize_blockwise(_dev_ptr(code, torch.float32, "code"), _dev_ptr(x, torch.float32, "x"),
+                                     _dev_ptr(absmax, torch.float32, "absmax"),
+                                     _dev_ptr(codes, torch.uint8, "codes"), n, blocksize, _stream(x.device)))
+    return absmax, codes
+
+
+def dequantize_blockwise(code: torch.Tensor, codes: torch.Tensor, absmax: torch.Tensor,
+                         out: torch.Tensor | None = None, blocksize: int = BLOCKSIZE):
+    n = codes.numel()
+    if out is None:
+        out = torch.empty(n, dtype=torch.float32, device=codes.device)
+    if out.numel() != n or absmax.numel() < nblocks(n, blocksize) or code.numel() != 256:
+        raise ValueError("size mismatch")
+    _check(lib.q8_dequantize_blockwise(_dev_ptr(code, torch.float32, "code"), _dev_ptr(codes, torch.uint8, "codes"),
+                                       _dev_ptr(absmax, torch.float32, "absmax"), _dev_ptr(out, torch.float32, "out"),
+                                       n, blocksize, _stream(codes.device)))
+    return out
+
+
+def hparams(lr, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, bias_correction=True) -> HParams:
+    return HParams(float(lr), float(beta1), float(beta2), float(eps), float(weight_decay),
+                   1 if bias_correction else 0)
+
+
+def optim8bit_step(kind, p, g, s1, s2, absmax1, absmax2, *, lr, beta1=0.9, beta2=0.999, eps=1e-8,
+                   weight_decay=0.0, bias_correction=True, step=1, blocksize=BLOCKSIZE, hp: HParams | None = None):
+    """One fused 8-bit step on a single flat tensor (in place)."""
+    kind = KINDS.get(kind, kind)
+    n = p.numel()
+    if g.numel() != n or s1.numel() != n or (kind != Q8_MOMENTUM and s2.numel() != n):
+        raise ValueError("size mismatch")
+    if g.dtype not in GDTYPES:
+        raise ValueError(f"unsupported gradient dtype {g.dtype}")
+    if hp is None:
+        hp = hparams(lr, beta1, beta2, eps, weight_decay, bias_correction)
+    _check(lib.q8_optim8bit_step(kind, _dev_ptr(p, torch.float32, "p"), _dev_ptr(g, None, "g"), GDTYPES[g.dtype],
+                                 _dev_ptr(s1, torch.uint8, "s1"), _dev_ptr(s2, torch.uint8, "s2"),
+                                 _dev_ptr(absmax1, torch.float32, "absmax1"),
+                                 _dev_ptr(absmax2, torch.float32, "absmax2"), n, blocksize, ctypes.byref(hp),
+                                 int(step), _stream(p.device)))
+
+
+class TensorList:
+    """A prepared (cached) host descriptor array for optim8bit_step_multi."""
+
+    def __init__(self, entries):
+        """entries: iterable of (p, g, s1, s2_or_None, absmax1, absmax2_or_None) CUDA tensors."""
+        entries = list(entries)
+        self.arr = (TensorDesc * max(1, len(entries)))()
+        self.count = len(entries)
+        self.gdtype = None
+        self.keep = entries  # keep tensors alive
+        for i, (p, g, s1, s2, a1, a2) in enumerate(entries):
+            n = p.numel()
+            if g.numel() != n or s1.numel() != n or (s2 is not None and s2.numel() != n):
+                raise ValueError(f"tensor {i}: size mismatch")
+            gd = GDTYPES[g.dtype]
+            if self.gdtype is None:
+                self.gdtype = gd
+            elif gd != self.gdtype:
+                raise ValueError("all gradients of one multi-tensor launch must share a dtype")
+            self.arr[i] = TensorDesc(_dev_ptr(p, torch.float32, "p"), _dev_ptr(g, None, "g"),
+                                     _dev_ptr(s1, torch.uint8, "s1"), _dev_ptr(s2, torch.uint8, "s2"),
+                                     _dev_ptr(a1, torch.float32, "absmax1"), _dev_ptr(a2, torch.float32, "absmax2"), n)
+        self.device = entries[0][0].device if entries else None
+
+
+def optim8bit_step_multi(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0,
+                         bias_correction=True, step=1, blocksize=BLOCKSIZE, hp: HParams | None = None):
+    """One fused 8-bit step over many tensors (one launch per <= 384 tensors)."""
+    kind = KINDS.get(kind, kind)
+    tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
+    if tl.count == 0:
+        return
+    if hp is None:
+        hp = hparams(lr, beta1, beta2, eps, weight_decay, bias_correction)
+    _check(lib.q8_optim8bit_step_multi(kind, tl.gdtype, tl.arr, tl.count, blocksize, ctypes.byref(hp), int(step),
+                                       _stream(tl.device)))

@@ -1,0 +1,296 @@
+// q8_api.cu -- the C ABI declared in include/q8.h: validation, host scalars, per-device
+// table cache and kernel launches.  No compute happens on the host except the once-per-
+// process codebook/threshold construction (a1) and the per-call fp32 scalars (G8-G10).
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/q8.h"
+#include "q8_kernels.cuh"
+
+namespace q8 {
+void build_dynamic_codebook(bool is_signed, float out[256]);
+void build_eytzinger_thresholds(const float Q[256], float out[256]);
+}  // namespace q8
+
+namespace {
+
+thread_local std::string g_last_error;
+
+q8_status fail(q8_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+q8_status ok() {
+    g_last_error.clear();
+    return Q8_OK;
+}
+
+q8_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(Q8_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+// ---------------------------------------------------------------- per-device state
+constexpr int kMaxDevices = 64;
+struct DeviceState {
+    float* tabs = nullptr;  // kTabFloats device floats
+    int sms = 0;
+};
+std::mutex g_mu;
+DeviceState g_dev[kMaxDevices];
+
+q8_status device_state(DeviceState** out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev < 0 || dev >= kMaxDevices) return fail(Q8_ERR_UNSUPPORTED, "device ordinal %d out of range", dev);
+    std::lock_guard<std::mutex> lock(g_mu);
+    DeviceState& d = g_dev[dev];
+    if (d.tabs == nullptr) {
+        float host[q8::kTabFloats];
+        q8::build_dynamic_codebook(true, host + q8::kTabQs);
+        q8::build_eytzinger_thresholds(host + q8::kTabQs, host + q8::kTabTs);
+        q8::build_dynamic_codebook(false, host + q8::kTabQu);
+        q8::build_eytzinger_thresholds(host + q8::kTabQu, host + q8::kTabTu);
+        float* ptr = nullptr;
+        e = cudaMalloc(&ptr, sizeof host);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(tables)");
+        e = cudaMemcpy(ptr, host, sizeof host, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(ptr);
+            return cuda_fail(e, "cudaMemcpy(tables)");
+        }
+        int sms = 0;
+        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) {
+            cudaFree(ptr);
+            return cuda_fail(e, "cudaDeviceGetAttribute");
+        }
+        d.sms = sms;
+        d.tabs = ptr;
+    }
+    *out = &d;
+    return Q8_OK;
+}
+
+// Resident CTAs per SM for a kernel (cached per function pointer by the caller).
+int ctas_per_sm(const void* fn) {
+    const char* env = std::getenv("Q8_CTAS_PER_SM");
+    if (env && std::atoi(env) > 0) return std::atoi(env);
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, q8::kThreads, 0) != cudaSuccess || occ < 1) occ = 1;
+    return occ;
+}
+
+int64_t grid_for(const DeviceState* d, int occ, int64_t nblocks) {
+    int64_t g = static_cast<int64_t>(d->sms) * occ;
+    return nblocks < g ? nblocks : g;
+}
+
+// ---------------------------------------------------------------- hparams
+q8_status validate_hparams(q8_kind kind, const q8_hparams* hp, int64_t step) {
+    if (!hp) return fail(Q8_ERR_INVALID, "hparams is NULL");
+    if (kind != Q8_ADAM && kind != Q8_ADAMW && kind != Q8_MOMENTUM) return fail(Q8_ERR_INVALID, "bad kind %d", kind);
+    if (!(hp->lr >= 0.0) || !std::isfinite(hp->lr)) return fail(Q8_ERR_INVALID, "lr must be finite and >= 0");
+    if (!(hp->beta1 >= 0.0 && hp->beta1 < 1.0)) return fail(Q8_ERR_INVALID, "beta1 must be in [0, 1)");
+    if (!(hp->weight_decay >= 0.0) || !std::isfinite(hp->weight_decay))
+        return fail(Q8_ERR_INVALID, "weight_decay must be finite and >= 0");
+    if (kind != Q8_MOMENTUM) {
+        if (!(hp->beta2 >= 0.0 && hp->beta2 < 1.0)) return fail(Q8_ERR_INVALID, "beta2 must be in [0, 1)");
+        if (!(hp->eps > 0.0) || !std::isfinite(hp->eps)) return fail(Q8_ERR_INVALID, "eps must be finite and > 0");
+    }
+    if (step < 1) return fail(Q8_ERR_INVALID, "step must be >= 1 (got %lld)", static_cast<long long>(step));
+    return Q8_OK;
+}
+
+// fp32 scalars of the update, computed in double and rounded once (G8-G10).
+q8::StepScalars make_scalars(const q8_hparams* hp, int64_t step) {
+    q8::StepScalars s;
+    s.lr = static_cast<float>(hp->lr);
+    s.beta1 = static_cast<float>(hp->beta1);
+    s.beta2 = static_cast<float>(hp->beta2);
+    s.omb1 = static_cast<float>(1.0 - hp->beta1);
+    s.omb2 = static_cast<float>(1.0 - hp->beta2);
+    if (hp->bias_correction) {
+        // Kingma & Ba's folded bias correction: alpha_t = alpha sqrt(1 - b2^t) / (1 - b1^t),
+        // eps_hat = eps sqrt(1 - b2^t)  (G8)
+        const double bc1 = 1.0 - std::pow(hp->beta1, static_cast<double>(step));
+        const double bc2 = 1.0 - std::pow(hp->beta2, static_cast<double>(step));
+        s.step_size = static_cast<float>(hp->lr * std::sqrt(bc2) / bc1);
+        s.eps_hat = static_cast<float>(hp->eps * std::sqrt(bc2));
+    } else {
+        s.step_size = static_cast<float>(hp->lr);
+        s.eps_hat = static_cast<float>(hp->eps);
+    }
+    s.wd = static_cast<float>(hp->weight_decay);
+    s.decay = static_cast<float>(1.0 - hp->lr * hp->weight_decay);
+    return s;
+}
+
+q8_status validate_tensor(q8_kind kind, q8_dtype gdt, const q8_tensor& t, int idx) {
+    if (t.n < 0) return fail(Q8_ERR_INVALID, "tensor %d: n < 0", idx);
+    if (t.n == 0) return Q8_OK;
+    const bool two = kind != Q8_MOMENTUM;
+    if (!t.p || !t.g || !t.s1 || !t.absmax1 || (two && (!t.s2 || !t.absmax2)))
+        return fail(Q8_ERR_INVALID, "tensor %d: NULL buffer with n > 0", idx);
+    if (!aligned(t.p, 16)) return fail(Q8_ERR_INVALID, "tensor %d: p not 16-byte aligned", idx);
+    if (!aligned(t.g, gdt == Q8_F32 ? 16 : 8)) return fail(Q8_ERR_INVALID, "tensor %d: g misaligned", idx);
+    if (!aligned(t.s1, 4) || (two && !aligned(t.s2, 4)))
+        return fail(Q8_ERR_INVALID, "tensor %d: codes not 4-byte aligned", idx);
+    if (!aligned(t.absmax1, 4) || (two && !aligned(t.absmax2, 4)))
+        return fail(Q8_ERR_INVALID, "tensor %d: absmax not 4-byte aligned", idx);
+    return Q8_OK;
+}
+
+// ---------------------------------------------------------------- launch dispatch
+template <int KIND, int GDT, int MAXT>
+q8_status launch_step(const q8::StepParams<MAXT>& P, const DeviceState* d, cudaStream_t st) {
+    auto fn = q8::optim8bit_step_kernel<KIND, GDT, MAXT>;
+    static int occ = ctas_per_sm(reinterpret_cast<const void*>(fn));
+    const int64_t grid = grid_for(d, occ, P.total_blocks);
+    fn<<<static_cast<unsigned>(grid), q8::kThreads, 0, st>>>(P, d->tabs);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "optim8bit_step_kernel launch");
+    return Q8_OK;
+}
+
+template <int MAXT>
+q8_status dispatch_step(q8_kind kind, q8_dtype gdt, const q8::StepParams<MAXT>& P, const DeviceState* d,
+                        cudaStream_t st) {
+#define Q8_CASE(K, G) \
+    if (kind == K && gdt == G) return launch_step<K, G, MAXT>(P, d, st);
+    Q8_CASE(Q8_ADAM, Q8_F32) Q8_CASE(Q8_ADAM, Q8_F16) Q8_CASE(Q8_ADAM, Q8_BF16)
+    Q8_CASE(Q8_ADAMW, Q8_F32) Q8_CASE(Q8_ADAMW, Q8_F16) Q8_CASE(Q8_ADAMW, Q8_BF16)
+    Q8_CASE(Q8_MOMENTUM, Q8_F32) Q8_CASE(Q8_MOMENTUM, Q8_F16) Q8_CASE(Q8_MOMENTUM, Q8_BF16)
+#undef Q8_CASE
+    return fail(Q8_ERR_INVALID, "bad kind/dtype");
+}
+
+q8_status check_common(q8_dtype gdt, int32_t blocksize) {
+    if (gdt != Q8_F32 && gdt != Q8_F16 && gdt != Q8_BF16) return fail(Q8_ERR_INVALID, "bad g_dtype %d", gdt);
+    if (blocksize != q8::kBlock)
+        return fail(Q8_ERR_UNSUPPORTED, "blocksize %d unsupported on the GPU (only 2048)", blocksize);
+    return Q8_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* q8_last_error(void) { return g_last_error.c_str(); }
+
+const char* q8_version(void) { return "q8 0.1 sm_100a"; }
+
+q8_status q8_create_dynamic_codebook(int32_t is_signed, float* out_host) {
+    if (!out_host) return fail(Q8_ERR_INVALID, "out_host is NULL");
+    q8::build_dynamic_codebook(is_signed != 0, out_host);
+    return ok();
+}
+
+q8_status q8_quantize_blockwise(const float* code_dev, const float* x_dev, float* absmax_dev, uint8_t* codes_dev,
+                                int64_t n, int32_t blocksize, void* stream) {
+    if (n < 0) return fail(Q8_ERR_INVALID, "n < 0");
+    if (blocksize != q8::kBlock) return fail(Q8_ERR_UNSUPPORTED, "blocksize %d unsupported (only 2048)", blocksize);
+    if (n == 0) return ok();
+    if (!code_dev || !x_dev || !absmax_dev || !codes_dev) return fail(Q8_ERR_INVALID, "NULL buffer with n > 0");
+    if (!aligned(x_dev, 16) || !aligned(codes_dev, 4) || !aligned(absmax_dev, 4) || !aligned(code_dev, 4))
+        return fail(Q8_ERR_INVALID, "misaligned buffer (x 16 B, codes 4 B)");
+    DeviceState* d = nullptr;
+    if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    const int64_t nb = (n + q8::kBlock - 1) / q8::kBlock;
+    static int occ = ctas_per_sm(reinterpret_cast<const void*>(q8::quantize_blockwise_kernel));
+    q8::quantize_blockwise_kernel<<<static_cast<unsigned>(grid_for(d, occ, nb)), q8::kThreads, 0,
+                                    static_cast<cudaStream_t>(stream)>>>(code_dev, x_dev, absmax_dev, codes_dev, n, nb);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "quantize_blockwise_kernel launch");
+    return ok();
+}
+
+q8_status q8_dequantize_blockwise(const float* code_dev, const uint8_t* codes_dev, const float* absmax_dev,
+                                  float* out_dev, int64_t n, int32_t blocksize, void* stream) {
+    if (n < 0) return fail(Q8_ERR_INVALID, "n < 0");
+    if (blocksize != q8::kBlock) return fail(Q8_ERR_UNSUPPORTED, "blocksize %d unsupported (only 2048)", blocksize);
+    if (n == 0) return ok();
+    if (!code_dev || !codes_dev || !absmax_dev || !out_dev) return fail(Q8_ERR_INVALID, "NULL buffer with n > 0");
+    if (!aligned(out_dev, 16) || !aligned(codes_dev, 4) || !aligned(absmax_dev, 4) || !aligned(code_dev, 4))
+        return fail(Q8_ERR_INVALID, "misaligned buffer (out 16 B, codes 4 B)");
+    DeviceState* d = nullptr;
+    if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    const int64_t nb = (n + q8::kBlock - 1) / q8::kBlock;
+    static int occ = ctas_per_sm(reinterpret_cast<const void*>(q8::dequantize_blockwise_kernel));
+    q8::dequantize_blockwise_kernel<<<static_cast<unsigned>(grid_for(d, occ, nb)), q8::kThreads, 0,
+                                      static_cast<cudaStream_t>(stream)>>>(code_dev, codes_dev, absmax_dev, out_dev, n,
+                                                                            nb);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "dequantize_blockwise_kernel launch");
+    return ok();
+}
+
+q8_status q8_optim8bit_step(q8_kind kind, float* p, const void* g, q8_dtype g_dtype, uint8_t* s1, uint8_t* s2,
+                            float* absmax1, float* absmax2, int64_t n, int32_t blocksize, const q8_hparams* hp,
+                            int64_t step, void* stream) {
+    if (q8_status s = check_common(g_dtype, blocksize); s != Q8_OK) return s;
+    if (q8_status s = validate_hparams(kind, hp, step); s != Q8_OK) return s;
+    q8_tensor t{p, g, s1, s2, absmax1, absmax2, n};
+    if (q8_status s = validate_tensor(kind, g_dtype, t, 0); s != Q8_OK) return s;
+    if (n == 0) return ok();
+    DeviceState* d = nullptr;
+    if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    q8::StepParams<1> P;
+    P.s = make_scalars(hp, step);
+    P.num_tensors = 1;
+    P.block_start[0] = 0;
+    P.total_blocks = P.block_start[1] = (n + q8::kBlock - 1) / q8::kBlock;
+    P.t[0] = q8::TensorDesc{p, g, s1, s2, absmax1, absmax2, n};
+    if (q8_status s = dispatch_step<1>(kind, g_dtype, P, d, static_cast<cudaStream_t>(stream)); s != Q8_OK) return s;
+    return ok();
+}
+
+q8_status q8_optim8bit_step_multi(q8_kind kind, q8_dtype g_dtype, const q8_tensor* tensors_host, int32_t num_tensors,
+                                  int32_t blocksize, const q8_hparams* hp, int64_t step, void* stream) {
+    if (q8_status s = check_common(g_dtype, blocksize); s != Q8_OK) return s;
+    if (q8_status s = validate_hparams(kind, hp, step); s != Q8_OK) return s;
+    if (num_tensors < 0) return fail(Q8_ERR_INVALID, "num_tensors < 0");
+    if (num_tensors > 0 && !tensors_host) return fail(Q8_ERR_INVALID, "tensors_host is NULL");
+    for (int i = 0; i < num_tensors; ++i)
+        if (q8_status s = validate_tensor(kind, g_dtype, tensors_host[i], i); s != Q8_OK) return s;
+    DeviceState* d = nullptr;
+    if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    constexpr int MAXT = Q8_MAX_TENSORS_PER_LAUNCH;
+    static thread_local q8::StepParams<MAXT> P;  // ~24 KB; kernel parameter (copied at launch)
+    P.s = make_scalars(hp, step);
+    int i = 0;
+    while (i < num_tensors) {
+        int k = 0;
+        int64_t blocks = 0;
+        for (; i < num_tensors && k < MAXT; ++i) {
+            const q8_tensor& t = tensors_host[i];
+            if (t.n == 0) continue;
+            P.t[k] = q8::TensorDesc{t.p, t.g, t.s1, t.s2, t.absmax1, t.absmax2, t.n};
+            P.block_start[k] = blocks;
+            blocks += (t.n + q8::kBlock - 1) / q8::kBlock;
+            ++k;
+        }
+        if (k == 0) break;
+        P.num_tensors = k;
+        P.block_start[k] = blocks;
+        P.total_blocks = blocks;
+        if (q8_status s = dispatch_step<MAXT>(kind, g_dtype, P, d, static_cast<cudaStream_t>(stream)); s != Q8_OK)
+            return s;
+    }
+    return ok();
+}
+
+}  // extern "C"

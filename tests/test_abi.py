@@ -1,0 +1,100 @@
+"""CPU-side checks of the C ABI (no GPU needed): libq8.so loads, exports every symbol that
+include/q8.h declares, its host codebook matches the oracle bit for bit, and argument
+validation fails synchronously with the documented status codes before touching CUDA."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2110_02861_b200 as q8
+from paper_2110_02861_b200 import _binding as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "q8.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(q8_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol():
+    syms = declared_symbols()
+    assert set(syms) == set(B.EXPORTS), syms
+    for s in syms:
+        assert hasattr(B.lib, s), s
+    out = os.popen(f"nm -D --defined-only {B.LIB_PATH}").read()
+    for s in syms:
+        assert re.search(rf"\bT {s}\b", out), s
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {B.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out), out
+
+
+@pytest.mark.parametrize("signed", [True, False])
+def test_host_codebook_matches_oracle(signed):
+    a = q8.create_dynamic_codebook(signed).numpy()
+    b = oracle.dynamic_codebook(signed)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def _hp(**kw):
+    d = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, bias_correction=True)
+    d.update(kw)
+    return B.hparams(**d)
+
+
+FAKE = 1 << 20  # an aligned non-NULL address; validation fails before any dereference
+
+
+@pytest.mark.parametrize("args,status", [
+    (dict(n=-1), B.Q8_ERR_INVALID),
+    (dict(blocksize=1024), B.Q8_ERR_UNSUPPORTED),
+    (dict(gdt=7), B.Q8_ERR_INVALID),
+    (dict(kind=9), B.Q8_ERR_INVALID),
+    (dict(p=0), B.Q8_ERR_INVALID),
+    (dict(p=FAKE + 4), B.Q8_ERR_INVALID),
+    (dict(s1=FAKE + 1), B.Q8_ERR_INVALID),
+    (dict(step=0), B.Q8_ERR_INVALID),
+    (dict(hp=_hp(beta1=1.0)), B.Q8_ERR_INVALID),
+    (dict(hp=_hp(eps=0.0)), B.Q8_ERR_INVALID),
+    (dict(hp=_hp(lr=-1.0)), B.Q8_ERR_INVALID),
+])
+def test_step_validation(args, status):
+    a = dict(kind=B.Q8_ADAM, p=FAKE, g=FAKE, gdt=B.Q8_BF16, s1=FAKE, s2=FAKE, a1=FAKE, a2=FAKE, n=4096,
+             blocksize=2048, hp=_hp(), step=1)
+    a.update(args)
+    rc = B.lib.q8_optim8bit_step(a["kind"], a["p"], a["g"], a["gdt"], a["s1"], a["s2"], a["a1"], a["a2"], a["n"],
+                                 a["blocksize"], ctypes.byref(a["hp"]), a["step"], None)
+    assert rc == status
+    assert B.lib.q8_last_error().decode() != ""
+
+
+def test_zero_length_is_noop_without_device():
+    rc = B.lib.q8_optim8bit_step(B.Q8_ADAM, 0, 0, B.Q8_F32, 0, 0, 0, 0, 0, 2048, ctypes.byref(_hp()), 1, None)
+    assert rc == B.Q8_OK
+    assert B.lib.q8_quantize_blockwise(0, 0, 0, 0, 0, 2048, None) == B.Q8_OK
+    assert B.lib.q8_dequantize_blockwise(0, 0, 0, 0, 0, 2048, None) == B.Q8_OK
+
+
+def test_codec_validation():
+    assert B.lib.q8_quantize_blockwise(FAKE, FAKE, FAKE, FAKE, -5, 2048, None) == B.Q8_ERR_INVALID
+    assert B.lib.q8_quantize_blockwise(FAKE, FAKE + 8, FAKE, FAKE, 10, 2048, None) == B.Q8_ERR_INVALID
+    assert B.lib.q8_dequantize_blockwise(FAKE, FAKE, FAKE, FAKE, 10, 512, None) == B.Q8_ERR_UNSUPPORTED
+    assert B.lib.q8_create_dynamic_codebook(1, None) == B.Q8_ERR_INVALID
+
+
+def test_multi_validation():
+    arr = (B.TensorDesc * 2)()
+    arr[0] = B.TensorDesc(FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 100)
+    arr[1] = B.TensorDesc(FAKE + 4, FAKE, FAKE, FAKE, FAKE, FAKE, 100)
+    rc = B.lib.q8_optim8bit_step_multi(B.Q8_ADAM, B.Q8_F16, arr, 2, 2048, ctypes.byref(_hp()), 1, None)
+    assert rc == B.Q8_ERR_INVALID and "tensor 1" in B.lib.q8_last_error().decode()
+    assert B.lib.q8_optim8bit_step_multi(B.Q8_ADAM, B.Q8_F16, arr, -1, 2048, ctypes.byref(_hp()), 1,
+                                         None) == B.Q8_ERR_INVALID
