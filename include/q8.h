@@ -91,6 +91,15 @@ q8_status q8_create_dynamic_codebook(int32_t is_signed, float* out_host);
 q8_status q8_quantize_blockwise(const float* code_dev, const float* x_dev, float* absmax_dev,
                                 uint8_t* codes_dev, int64_t n, int32_t blocksize, void* stream);
 
+/* Block-wise quantization with the library's built-in dynamic data type (is_signed = 1:
+ * the signed table of q8_create_dynamic_codebook(1); 0: the unsigned one), computed by the
+ * same normalization and nearest-code search as q8_optim8bit_step (bucketed search,
+ * DESIGN.md 6.2).  Results are identical to q8_quantize_blockwise with that table copied to
+ * the device (Eq.4; ties to the lower index).  For is_signed = 0 negative inputs get code 0.
+ * Buffers and errors as q8_quantize_blockwise. */
+q8_status q8_quantize_blockwise_dynamic(int32_t is_signed, const float* x_dev, float* absmax_dev,
+                                        uint8_t* codes_dev, int64_t n, int32_t blocksize, void* stream);
+
 /* Block-wise dequantization: out_i = code_dev[codes_i] * absmax_dev[i / B] (one fp32
  * multiply).  codes_dev [n] uint8 4-B aligned, absmax_dev [ceil(n/B)], out_dev [n] fp32 16-B
  * aligned.  blocksize must be 2048. */

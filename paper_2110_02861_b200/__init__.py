@@ -7,10 +7,10 @@ optimizer classes and the ZeRO-1 sharding wrapper.  There is no CPU fallback.
 """
 from ._binding import (BLOCKSIZE, MAX_TENSORS_PER_LAUNCH, Q8Error, TensorList, create_dynamic_codebook,
                        dequantize_blockwise, hparams, nblocks, optim8bit_step, optim8bit_step_multi,
-                       quantize_blockwise, version)
+                       quantize_blockwise, quantize_blockwise_dynamic, version)
 
 __all__ = [
     "BLOCKSIZE", "MAX_TENSORS_PER_LAUNCH", "Q8Error", "TensorList", "create_dynamic_codebook",
     "dequantize_blockwise", "hparams", "nblocks", "optim8bit_step", "optim8bit_step_multi", "quantize_blockwise",
-    "version",
+    "quantize_blockwise_dynamic", "version",
 ]

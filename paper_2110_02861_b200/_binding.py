@@ -20,7 +20,8 @@ BLOCKSIZE = 2048
 KINDS = {"adam": Q8_ADAM, "adamw": Q8_ADAMW, "momentum": Q8_MOMENTUM}
 GDTYPES = {torch.float32: Q8_F32, torch.float16: Q8_F16, torch.bfloat16: Q8_BF16}
 
-EXPORTS = ("q8_create_dynamic_codebook", "q8_quantize_blockwise", "q8_dequantize_blockwise",
+EXPORTS = ("q8_create_dynamic_codebook", "q8_quantize_blockwise", "q8_quantize_blockwise_dynamic",
+           "q8_dequantize_blockwise",
            "q8_optim8bit_step", "q8_optim8bit_step_multi", "q8_last_error", "q8_version")
 
 
@@ -47,6 +48,7 @@ def _load():
     vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
     lib.q8_create_dynamic_codebook.argtypes = [i32, vp]
     lib.q8_quantize_blockwise.argtypes = [vp, vp, vp, vp, i64, i32, vp]
+    lib.q8_quantize_blockwise_dynamic.argtypes = [i32, vp, vp, vp, i64, i32, vp]
     lib.q8_dequantize_blockwise.argtypes = [vp, vp, vp, vp, i64, i32, vp]
     lib.q8_optim8bit_step.argtypes = [i32, vp, vp, i32, vp, vp, vp, vp, i64, i32, ctypes.POINTER(HParams), i64, vp]
     lib.q8_optim8bit_step_multi.argtypes = [i32, i32, ctypes.POINTER(TensorDesc), i32, i32,
@@ -109,6 +111,22 @@ def quantize_blockwise(code: torch.Tensor, x: torch.Tensor, absmax: torch.Tensor
     _check(lib.q8_quantize_blockwise(_dev_ptr(code, torch.float32, "code"), _dev_ptr(x, torch.float32, "x"),
                                      _dev_ptr(absmax, torch.float32, "absmax"),
                                      _dev_ptr(codes, torch.uint8, "codes"), n, blocksize, _stream(x.device)))
+    return absmax, codes
+
+
+def quantize_blockwise_dynamic(signed: bool, x: torch.Tensor, absmax: torch.Tensor | None = None,
+                               codes: torch.Tensor | None = None, blocksize: int = BLOCKSIZE):
+    """Eq.4 with the library's built-in dynamic data type (the step kernel's search path)."""
+    n = x.numel()
+    if absmax is None:
+        absmax = torch.empty(nblocks(n, blocksize), dtype=torch.float32, device=x.device)
+    if codes is None:
+        codes = torch.empty(n, dtype=torch.uint8, device=x.device)
+    if codes.numel() != n or absmax.numel() < nblocks(n, blocksize):
+        raise ValueError("size mismatch")
+    _check(lib.q8_quantize_blockwise_dynamic(1 if signed else 0, _dev_ptr(x, torch.float32, "x"),
+                                             _dev_ptr(absmax, torch.float32, "absmax"),
+                                             _dev_ptr(codes, torch.uint8, "codes"), n, blocksize, _stream(x.device)))
     return absmax, codes
 
 

@@ -12,6 +12,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 
 namespace q8 {
 
@@ -60,6 +61,51 @@ void build_eytzinger_thresholds(const float Q[256], float out[256]) {
         const int k = eytzinger_rank(i);
         out[i] = midpoint_round_down(Q[k], Q[k + 1]);
     }
+}
+
+// Sorted thresholds: out[k] = T_k for k = 0..254, out[255] = +inf (so c0 = 255 never moves).
+void build_sorted_thresholds(const float Q[256], float out[256]) {
+    for (int k = 0; k < 255; ++k) out[k] = midpoint_round_down(Q[k], Q[k + 1]);
+    out[255] = INFINITY;
+}
+
+static float bits_to_float(uint32_t u) {
+    float f;
+    std::memcpy(&f, &u, sizeof f);
+    return f;
+}
+
+// code(y) = #{k : y > T_k}  (= Eq.3 argmin with lower-index ties, see above)
+static int code_of(const float T[256], float y) {
+    int c = 0;
+    while (c < 255 && y > T[c]) ++c;
+    return c;
+}
+
+// Bucket tables of the bucketed search (q8_kernels.cuh "Bucketed search").  Bucket mk covers
+// the fp32 magnitudes whose bits lie in [(mk + base) << shift, (mk + base + 1) << shift),
+// where base = bits(2^-22) >> shift, clamped to [0, 1]; bucket 0 also holds every magnitude
+// below 2^-22.  lut[key] = smallest code in the bucket.  Returns false if some bucket spans
+// more than two codes (then the one-compare finish would be wrong).
+bool build_bucket_lut(const float T[256], bool is_signed, uint32_t min_mag_bits, int shift, int nbuckets,
+                      int neg_offset, uint8_t* lut, int lut_bytes) {
+    std::memset(lut, 0, static_cast<size_t>(lut_bytes));
+    const uint32_t base = min_mag_bits >> shift;
+    for (int mk = 0; mk < nbuckets; ++mk) {
+        uint32_t lo = (mk == 0) ? 0u : ((base + static_cast<uint32_t>(mk)) << shift);
+        uint32_t hi = ((base + static_cast<uint32_t>(mk) + 1u) << shift) - 1u;
+        if (hi > 0x3f800000u) hi = 0x3f800000u;
+        const float flo = bits_to_float(lo), fhi = bits_to_float(hi);
+        int c_lo = code_of(T, flo), c_hi = code_of(T, fhi);
+        if (c_hi - c_lo > 1 || mk >= lut_bytes) return false;
+        lut[mk] = static_cast<uint8_t>(c_lo);
+        if (is_signed) {
+            const int c_nlo = code_of(T, -fhi), c_nhi = code_of(T, -flo);
+            if (c_nhi - c_nlo > 1 || neg_offset + mk >= lut_bytes) return false;
+            lut[neg_offset + mk] = static_cast<uint8_t>(c_nlo);
+        }
+    }
+    return true;
 }
 
 }  // namespace q8

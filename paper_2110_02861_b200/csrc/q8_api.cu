@@ -15,6 +15,9 @@
 namespace q8 {
 void build_dynamic_codebook(bool is_signed, float out[256]);
 void build_eytzinger_thresholds(const float Q[256], float out[256]);
+void build_sorted_thresholds(const float Q[256], float out[256]);
+bool build_bucket_lut(const float T[256], bool is_signed, uint32_t min_mag_bits, int shift, int nbuckets,
+                      int neg_offset, uint8_t* lut, int lut_bytes);
 }  // namespace q8
 
 namespace {
@@ -59,11 +62,19 @@ q8_status device_state(DeviceState** out) {
     std::lock_guard<std::mutex> lock(g_mu);
     DeviceState& d = g_dev[dev];
     if (d.tabs == nullptr) {
-        float host[q8::kTabFloats];
+        static float host[q8::kTabFloats];
         q8::build_dynamic_codebook(true, host + q8::kTabQs);
         q8::build_eytzinger_thresholds(host + q8::kTabQs, host + q8::kTabTs);
+        q8::build_sorted_thresholds(host + q8::kTabQs, host + q8::kTabSs);
         q8::build_dynamic_codebook(false, host + q8::kTabQu);
         q8::build_eytzinger_thresholds(host + q8::kTabQu, host + q8::kTabTu);
+        q8::build_sorted_thresholds(host + q8::kTabQu, host + q8::kTabSu);
+        uint8_t* lut = reinterpret_cast<uint8_t*>(host + q8::kTabLut);
+        if (!q8::build_bucket_lut(host + q8::kTabSs, true, q8::kMinMagBits, q8::kShiftS, q8::kBucketsS, q8::kNegOffS,
+                                  lut, q8::kLutSBytes) ||
+            !q8::build_bucket_lut(host + q8::kTabSu, false, q8::kMinMagBits, q8::kShiftU, q8::kBucketsU, 0,
+                                  lut + q8::kLutSBytes, q8::kLutUBytes))
+            return fail(Q8_ERR_CUDA, "internal: bucket table spans more than two codes");
         float* ptr = nullptr;
         e = cudaMalloc(&ptr, sizeof host);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(tables)");
@@ -155,15 +166,29 @@ q8_status validate_tensor(q8_kind kind, q8_dtype gdt, const q8_tensor& t, int id
 }
 
 // ---------------------------------------------------------------- launch dispatch
-template <int KIND, int GDT, int MAXT>
-q8_status launch_step(const q8::StepParams<MAXT>& P, const DeviceState* d, cudaStream_t st) {
-    auto fn = q8::optim8bit_step_kernel<KIND, GDT, MAXT>;
+int search_variant() {
+    static const int v = [] {
+        const char* env = std::getenv("Q8_SEARCH");
+        return (env && std::strcmp(env, "eytzinger") == 0) ? q8::SEARCH_EYTZINGER : q8::SEARCH_BUCKET;
+    }();
+    return v;
+}
+
+template <int KIND, int GDT, int MAXT, int SEARCH>
+q8_status launch_step_v(const q8::StepParams<MAXT>& P, const DeviceState* d, cudaStream_t st) {
+    auto fn = q8::optim8bit_step_kernel<KIND, GDT, MAXT, SEARCH>;
     static int occ = ctas_per_sm(reinterpret_cast<const void*>(fn));
     const int64_t grid = grid_for(d, occ, P.total_blocks);
     fn<<<static_cast<unsigned>(grid), q8::kThreads, 0, st>>>(P, d->tabs);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "optim8bit_step_kernel launch");
     return Q8_OK;
+}
+
+template <int KIND, int GDT, int MAXT>
+q8_status launch_step(const q8::StepParams<MAXT>& P, const DeviceState* d, cudaStream_t st) {
+    if (search_variant() == q8::SEARCH_EYTZINGER) return launch_step_v<KIND, GDT, MAXT, q8::SEARCH_EYTZINGER>(P, d, st);
+    return launch_step_v<KIND, GDT, MAXT, q8::SEARCH_BUCKET>(P, d, st);
 }
 
 template <int MAXT>
@@ -215,6 +240,34 @@ q8_status q8_quantize_blockwise(const float* code_dev, const float* x_dev, float
                                     static_cast<cudaStream_t>(stream)>>>(code_dev, x_dev, absmax_dev, codes_dev, n, nb);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "quantize_blockwise_kernel launch");
+    return ok();
+}
+
+q8_status q8_quantize_blockwise_dynamic(int32_t is_signed, const float* x_dev, float* absmax_dev, uint8_t* codes_dev,
+                                        int64_t n, int32_t blocksize, void* stream) {
+    if (n < 0) return fail(Q8_ERR_INVALID, "n < 0");
+    if (blocksize != q8::kBlock) return fail(Q8_ERR_UNSUPPORTED, "blocksize %d unsupported (only 2048)", blocksize);
+    if (n == 0) return ok();
+    if (!x_dev || !absmax_dev || !codes_dev) return fail(Q8_ERR_INVALID, "NULL buffer with n > 0");
+    if (!aligned(x_dev, 16) || !aligned(codes_dev, 4) || !aligned(absmax_dev, 4))
+        return fail(Q8_ERR_INVALID, "misaligned buffer (x 16 B, codes 4 B)");
+    DeviceState* d = nullptr;
+    if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    const int64_t nb = (n + q8::kBlock - 1) / q8::kBlock;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (is_signed) {
+        static int occ = ctas_per_sm(reinterpret_cast<const void*>(q8::quantize_blockwise_dynamic_kernel<true>));
+        q8::quantize_blockwise_dynamic_kernel<true>
+            <<<static_cast<unsigned>(grid_for(d, occ, nb)), q8::kThreads, 0, st>>>(d->tabs, x_dev, absmax_dev,
+                                                                                   codes_dev, n, nb);
+    } else {
+        static int occ = ctas_per_sm(reinterpret_cast<const void*>(q8::quantize_blockwise_dynamic_kernel<false>));
+        q8::quantize_blockwise_dynamic_kernel<false>
+            <<<static_cast<unsigned>(grid_for(d, occ, nb)), q8::kThreads, 0, st>>>(d->tabs, x_dev, absmax_dev,
+                                                                                   codes_dev, n, nb);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "quantize_blockwise_dynamic_kernel launch");
     return ok();
 }
 

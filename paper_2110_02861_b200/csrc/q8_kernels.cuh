@@ -29,12 +29,34 @@ constexpr int kWarps = kThreads / 32;
 enum { KIND_ADAM = 0, KIND_ADAMW = 1, KIND_MOMENTUM = 2 };
 enum { G_F32 = 0, G_F16 = 1, G_BF16 = 2 };
 
-// Device-resident immutable tables (built on the host, codebook_host.cpp):
-//   [0,256)   Q_s  signed dynamic tree codebook, ascending
-//   [256,512) T_s  signed thresholds, Eytzinger order (slot 0 unused)
-//   [512,768) Q_u  unsigned dynamic codebook, ascending
-//   [768,1024)T_u  unsigned thresholds, Eytzinger order
-constexpr int kTabQs = 0, kTabTs = 256, kTabQu = 512, kTabTu = 768, kTabFloats = 1024;
+// Device-resident immutable tables (built on the host, codebook_host.cpp), as fp32 words:
+//   [0,256)     Q_s   signed dynamic tree codebook, ascending
+//   [256,512)   E_s   signed thresholds, Eytzinger order (slot 0 unused)
+//   [512,768)   Q_u   unsigned dynamic codebook, ascending
+//   [768,1024)  E_u   unsigned thresholds, Eytzinger order
+//   [1024,1280) S_s   signed thresholds T_k in sorted order, S_s[255] = +inf
+//   [1280,1536) S_u   unsigned thresholds, sorted, S_u[255] = +inf
+//   [1536,...)  bucket tables (uint8), see "bucketed search" below
+constexpr int kTabQs = 0, kTabTs = 256, kTabQu = 512, kTabTu = 768, kTabSs = 1024, kTabSu = 1280;
+constexpr int kTabLut = 1536;                     // word offset of the byte tables
+
+// Bucketed search.  The binary search's first seven levels are replaced by
+// one table lookup indexed by the leading bits of y, the eighth by a compare:
+//   signed:   mag = |y| bits clamped below at 2^-22;  mk = (mag >> 17) - (2^-22 bits >> 17)
+//             (exponent + 6 mantissa bits, 1409 buckets over [0, 1]); key = mk + 1536*[y < 0]
+//   unsigned: mk = (max(bits, 2^-22 bits) >> 16) - (2^-22 bits >> 16)  (7 mantissa bits, 2817)
+// LUT[key] = c0 = the smallest code in the bucket.  Every bucket spans at most two codes
+// (verified exhaustively at table-build time), so code = c0 + [y > T_{c0}]  (T sorted).
+constexpr uint32_t kMinMagBits = (127u - 22u) << 23;   // 2^-22: below every |threshold| (>= 1.6e-7)
+constexpr int kShiftS = 17, kShiftU = 16;
+constexpr int kBucketsS = ((0x3f800000 >> kShiftS) - (kMinMagBits >> kShiftS)) + 1;  // 1409
+constexpr int kBucketsU = ((0x3f800000 >> kShiftU) - (kMinMagBits >> kShiftU)) + 1;  // 2817
+constexpr int kNegOffS = 1536;
+constexpr int kLutSBytes = 3072;                   // [0,1409) y >= 0, [1536, 2945) y < 0
+constexpr int kLutUBytes = 2944;                   // 2817 used, padded to a multiple of 128
+constexpr int kTabBytes = kTabLut * 4 + kLutSBytes + kLutUBytes;
+constexpr int kTabFloats = kTabBytes / 4;
+constexpr int SEARCH_EYTZINGER = 0, SEARCH_BUCKET = 1;
 
 struct TensorDesc {
     float* p;
@@ -108,6 +130,28 @@ __device__ __forceinline__ uint32_t eytzinger_search(const float* __restrict__ T
 #pragma unroll
     for (int l = 0; l < 8; ++l) i = 2u * i + (y > T[i] ? 1u : 0u);
     return i - 256u;
+}
+
+// Bucketed nearest code: LUT lookup replaces levels 1-7 of the binary
+// search, one compare against the sorted threshold T_{c0} is level 8.  Keys are clamped so a
+// non-finite y (out of contract) can never index outside the tables.
+__device__ __forceinline__ uint32_t bucket_search_signed(const uint8_t* __restrict__ lut,
+                                                         const float* __restrict__ T, float y) {
+    const uint32_t u = __float_as_uint(y);
+    const uint32_t mag = min(max(u & 0x7fffffffu, kMinMagBits), 0x3f800000u);
+    const uint32_t key = (mag >> kShiftS) - (kMinMagBits >> kShiftS) + ((u & 0x80000000u) ? kNegOffS : 0u);
+    const uint32_t c0 = lut[key];
+    return c0 + (y > T[c0] ? 1u : 0u);
+}
+
+__device__ __forceinline__ uint32_t bucket_search_unsigned(const uint8_t* __restrict__ lut,
+                                                           const float* __restrict__ T, float y) {
+    // signed clamp: negative y (sign bit set) joins bucket 0, whose nearest code is Q_u[0] = 0
+    const int32_t u = min(max(static_cast<int32_t>(__float_as_uint(y)), static_cast<int32_t>(kMinMagBits)),
+                          static_cast<int32_t>(0x3f800000));
+    const uint32_t key = (static_cast<uint32_t>(u) >> kShiftU) - (kMinMagBits >> kShiftU);
+    const uint32_t c0 = lut[key];
+    return c0 + (y > T[c0] ? 1u : 0u);
 }
 
 // ---------------------------------------------------------------------------- reduction
@@ -194,22 +238,58 @@ __device__ __forceinline__ int find_tensor(const StepParams<MAXT>& P, int64_t b)
     }
 }
 
+// Shared-memory image of the tables one step kernel needs.
+template <int SEARCH>
+struct StepSmem {
+    float qs[256], qu[256];                          // decode tables Q_s, Q_u
+    float ts[256], tu[256];                          // thresholds: Eytzinger or sorted order
+    uint8_t lut_s[SEARCH == SEARCH_BUCKET ? kLutSBytes : 4];
+    uint8_t lut_u[SEARCH == SEARCH_BUCKET ? kLutUBytes : 4];
+};
+
+template <int SEARCH, bool kTwo>
+__device__ __forceinline__ void stage_step_tables(StepSmem<SEARCH>& sm, const float* __restrict__ tabs) {
+    const int tid = threadIdx.x;
+    sm.qs[tid] = tabs[kTabQs + tid];
+    sm.ts[tid] = tabs[(SEARCH == SEARCH_BUCKET ? kTabSs : kTabTs) + tid];
+    if constexpr (kTwo) {
+        sm.qu[tid] = tabs[kTabQu + tid];
+        sm.tu[tid] = tabs[(SEARCH == SEARCH_BUCKET ? kTabSu : kTabTu) + tid];
+    }
+    if constexpr (SEARCH == SEARCH_BUCKET) {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(tabs + kTabLut);
+        uint32_t* dst_s = reinterpret_cast<uint32_t*>(sm.lut_s);
+        for (int i = tid; i < kLutSBytes / 4; i += kThreads) dst_s[i] = src[i];
+        if constexpr (kTwo) {
+            uint32_t* dst_u = reinterpret_cast<uint32_t*>(sm.lut_u);
+            for (int i = tid; i < kLutUBytes / 4; i += kThreads) dst_u[i] = src[kLutSBytes / 4 + i];
+        }
+    }
+    __syncthreads();
+}
+
+template <int SEARCH>
+__device__ __forceinline__ uint32_t nearest_s(const StepSmem<SEARCH>& sm, float y) {
+    if constexpr (SEARCH == SEARCH_BUCKET) return bucket_search_signed(sm.lut_s, sm.ts, y);
+    else return eytzinger_search(sm.ts, y);
+}
+
+template <int SEARCH>
+__device__ __forceinline__ uint32_t nearest_u(const StepSmem<SEARCH>& sm, float y) {
+    if constexpr (SEARCH == SEARCH_BUCKET) return bucket_search_unsigned(sm.lut_u, sm.tu, y);
+    else return eytzinger_search(sm.tu, y);
+}
+
 // The fused step (S3; Fig.1): dequantize -> fp32 update -> block absmax ->
 // requantize, all in registers; each HBM byte is read once and written once.
-template <int KIND, int GDT, int MAXT>
+template <int KIND, int GDT, int MAXT, int SEARCH>
 __global__ void __launch_bounds__(kThreads) optim8bit_step_kernel(const __grid_constant__ StepParams<MAXT> P,
                                                                   const float* __restrict__ tabs) {
     constexpr bool kTwo = (KIND != KIND_MOMENTUM);
-    __shared__ float sQs[256], sTs[256], sQu[256], sTu[256];
+    __shared__ __align__(16) StepSmem<SEARCH> sm;
     __shared__ float red[2][2][kWarps];
     const int tid = threadIdx.x;
-    sQs[tid] = tabs[kTabQs + tid];
-    sTs[tid] = tabs[kTabTs + tid];
-    if constexpr (kTwo) {
-        sQu[tid] = tabs[kTabQu + tid];
-        sTu[tid] = tabs[kTabTu + tid];
-    }
-    __syncthreads();
+    stage_step_tables<SEARCH, kTwo>(sm, tabs);
     const StepScalars& S = P.s;
 
     int parity = 0;
@@ -248,8 +328,8 @@ __global__ void __launch_bounds__(kThreads) optim8bit_step_kernel(const __grid_c
             }
 #pragma unroll
             for (int e = 0; e < kVec; ++e) {
-                m[c][e] = __fmul_rn(sQs[(c1[c] >> (8 * e)) & 0xffu], N1old);
-                r[c][e] = kTwo ? __fmul_rn(sQu[(c2[c] >> (8 * e)) & 0xffu], N2old) : 0.0f;
+                m[c][e] = __fmul_rn(sm.qs[(c1[c] >> (8 * e)) & 0xffu], N1old);
+                r[c][e] = kTwo ? __fmul_rn(sm.qu[(c2[c] >> (8 * e)) & 0xffu], N2old) : 0.0f;
             }
         }
 
@@ -292,8 +372,8 @@ __global__ void __launch_bounds__(kThreads) optim8bit_step_kernel(const __grid_c
             uint32_t o1 = 0u, o2 = 0u;
 #pragma unroll
             for (int e = 0; e < kVec; ++e) {
-                o1 |= eytzinger_search(sTs, nz1(m[c][e])) << (8 * e);
-                if (kTwo) o2 |= eytzinger_search(sTu, nz2(r[c][e])) << (8 * e);
+                o1 |= nearest_s<SEARCH>(sm, nz1(m[c][e])) << (8 * e);
+                if (kTwo) o2 |= nearest_u<SEARCH>(sm, nz2(r[c][e])) << (8 * e);
             }
             if (full) {
                 st_stream_f4(T.p + i0, make_float4(w[c][0], w[c][1], w[c][2], w[c][3]));
@@ -389,6 +469,66 @@ __global__ void __launch_bounds__(kThreads) quantize_blockwise_kernel(const floa
             }
         }
         if (tid == 0) absmax[b] = N;
+    }
+}
+
+// Block-wise quantization with the library's own dynamic data type (signed P:90 or unsigned
+// P:118): same normalization (Normalizer) and bucketed search as the fused step kernel.
+template <bool kSigned>
+__global__ void __launch_bounds__(kThreads) quantize_blockwise_dynamic_kernel(const float* __restrict__ tabs,
+                                                                              const float* __restrict__ x,
+                                                                              float* __restrict__ absmax,
+                                                                              uint8_t* __restrict__ codes, int64_t n,
+                                                                              int64_t nblocks) {
+    __shared__ float sT[256];
+    __shared__ __align__(16) uint8_t sLut[kSigned ? kLutSBytes : kLutUBytes];
+    __shared__ float red[2][kWarps];
+    const int tid = threadIdx.x;
+    sT[tid] = tabs[(kSigned ? kTabSs : kTabSu) + tid];
+    {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(tabs + kTabLut) + (kSigned ? 0 : kLutSBytes / 4);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(sLut);
+        for (int i = tid; i < (kSigned ? kLutSBytes : kLutUBytes) / 4; i += kThreads) dst[i] = src[i];
+    }
+    __syncthreads();
+    int parity = 0;
+    for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, parity ^= 1) {
+        const int64_t base = b * kBlock;
+        const bool full = base + kBlock <= n;
+        float v[kGroups][kVec];
+        float mx = 0.0f;
+#pragma unroll
+        for (int c = 0; c < kGroups; ++c) {
+            const int64_t i0 = base + c * (kThreads * kVec) + tid * kVec;
+            if (full) {
+                float4 xv = ld_stream_f4(x + i0);
+                v[c][0] = xv.x; v[c][1] = xv.y; v[c][2] = xv.z; v[c][3] = xv.w;
+            } else {
+#pragma unroll
+                for (int e = 0; e < kVec; ++e) v[c][e] = (i0 + e < n) ? x[i0 + e] : 0.0f;
+            }
+#pragma unroll
+            for (int e = 0; e < kVec; ++e) mx = fmaxf(mx, fabsf(v[c][e]));
+        }
+        const Normalizer nz(block_max(mx, red[parity]));
+#pragma unroll
+        for (int c = 0; c < kGroups; ++c) {
+            const int64_t i0 = base + c * (kThreads * kVec) + tid * kVec;
+            uint32_t o = 0u;
+#pragma unroll
+            for (int e = 0; e < kVec; ++e) {
+                const float y = nz(v[c][e]);
+                o |= (kSigned ? bucket_search_signed(sLut, sT, y) : bucket_search_unsigned(sLut, sT, y)) << (8 * e);
+            }
+            if (full) {
+                st_stream_u32(codes + i0, o);
+            } else {
+#pragma unroll
+                for (int e = 0; e < kVec; ++e)
+                    if (i0 + e < n) codes[i0 + e] = static_cast<uint8_t>(o >> (8 * e));
+            }
+        }
+        if (tid == 0) absmax[b] = nz.N;
     }
 }
 

@@ -57,6 +57,19 @@ def test_quantize_dequantize_bit_exact(q8, n, signed):
     assert_same(c_g, c_r, "codes")
     d_g = q8.dequantize_blockwise(code_dev, c_g, a_g)
     assert_same(d_g, oracle.dequantize_blockwise(Q, c_r, a_r), "dequantized")
+    a_d, c_d = q8.quantize_blockwise_dynamic(signed, x.to(DEV))
+    assert_same(a_d, a_r, "absmax (dynamic)")
+    assert_same(c_d, c_r, "codes (dynamic)")
+
+
+def test_quantize_dynamic_unsigned_negative_inputs(q8):
+    """Unsigned table, negative inputs: the nearest code is Q_u[0] = 0 (Eq.3)."""
+    Q = oracle.dynamic_codebook(False)
+    x = synth.params(3 * 2048 + 11, seed=5, std=1.0)
+    a_r, c_r = oracle.quantize_blockwise(Q, x.numpy())
+    a_d, c_d = q8.quantize_blockwise_dynamic(False, x.to(DEV))
+    assert_same(a_d, a_r, "absmax")
+    assert_same(c_d, c_r, "codes")
 
 
 def _boundaries(Q):
@@ -84,12 +97,15 @@ def _boundaries(Q):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("path", ["generic", "dynamic"])
 @pytest.mark.parametrize("signed", [True, False])
-def test_nearest_code_exhaustive_fp32(q8, signed):
+def test_nearest_code_exhaustive_fp32(q8, signed, path):
     """Every finite fp32 y in [-1, 1] (signed) / [0, 1] (unsigned) through the public
-    quantize_blockwise: one +1.0 per 2048-block makes N_b = 1, so y/N_b = y exactly and the
-    codes are the nearest codes.  Expected: the oracle's step function, evaluated with
-    torch.searchsorted over its 255 decision boundaries."""
+    quantize_blockwise (generic table: Eytzinger 8-step search) and quantize_blockwise_dynamic
+    (built-in table: the step kernel's bucketed search): one +1.0 per 2048-block makes
+    N_b = 1, so y/N_b = y exactly and the codes are the nearest codes.  Expected: the
+    oracle's step function, evaluated with torch.searchsorted over its 255 decision
+    boundaries."""
     Q = oracle.dynamic_codebook(signed)
     bnd = torch.from_numpy(_boundaries(Q)).to(DEV)
     code_dev = torch.from_numpy(Q).to(DEV)
@@ -109,7 +125,10 @@ def test_nearest_code_exhaustive_fp32(q8, signed):
             flat = torch.zeros(nb * 2047, dtype=torch.float32, device=DEV)
             flat[:y.numel()] = y
             xv[:, 1:] = flat.view(nb, 2047)
-            a, c = q8.quantize_blockwise(code_dev, x)
+            if path == "generic":
+                a, c = q8.quantize_blockwise(code_dev, x)
+            else:
+                a, c = q8.quantize_blockwise_dynamic(signed, x)
             assert torch.all(a == 1.0)
             got = c.view(nb, 2048)[:, 1:].reshape(-1)[:y.numel()].to(torch.int64)
             exp = torch.searchsorted(bnd, y.to(torch.float64), right=True)
@@ -252,6 +271,20 @@ def test_multi_tensor_many_launches_and_empty(q8):
             oracle.optim8bit_step("adam", p, g, s1, s2, a1, a2, step=4, **hp)
         for k, (gt, rt) in enumerate(zip((e[0], e[2], e[3], e[4], e[5]), (p, s1, s2, a1, a2))):
             assert_same(gt, rt, f"t{i}.{k}")
+
+
+def test_eytzinger_step_variant_bit_exact():
+    """The pure 8-step Eytzinger search variant of the step kernel (Q8_SEARCH=eytzinger)
+    passes the same single-step parity cases (separate process: the variant is chosen once
+    per process)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, Q8_SEARCH="eytzinger")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k",
+                        "test_step_single_bit_exact or test_ten_steps or test_multi_tensor_resnet50"],
+                       env=env, capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
 def test_errors_surface_as_exceptions(q8):
