@@ -59,7 +59,7 @@ typedef struct {
 } q8_hparams;
 
 /* One tensor of a multi-tensor step (all device pointers; s2/absmax2 may be NULL for
- * Q8_MOMENTUM).  Alignment: p 16 B, g 16 B (fp32) / 8 B (16-bit), s1/s2 4 B. */
+ * Q8_MOMENTUM).  Alignment: p, g, s1, s2 16 B (TMA bulk copies). */
 typedef struct {
     float* p;
     const void* g;
@@ -117,8 +117,8 @@ q8_status q8_dequantize_blockwise(const float* code_dev, const uint8_t* codes_de
  *      Q_u (unsigned) (Eq.4, G14)
  * Arguments (device pointers unless noted):
  *   p        [n] fp32 parameters, read-modify-write, 16-B aligned
- *   g        [n] gradients of g_dtype (fp32 16-B aligned, fp16/bf16 8-B aligned), read
- *   s1, s2   [n] uint8 codes (state 1 / state 2), RMW, 4-B aligned; s2 unused (may be
+ *   g        [n] gradients of g_dtype, read, 16-B aligned
+ *   s1, s2   [n] uint8 codes (state 1 / state 2), RMW, 16-B aligned; s2 unused (may be
  *            NULL) for Q8_MOMENTUM.  All-zero codes+absmax is the valid initial state.
  *   absmax1, absmax2  [ceil(n/2048)] fp32, RMW; absmax2 unused for Q8_MOMENTUM
  *   blocksize must be 2048; step = t >= 1, the 1-based index of this update (the caller

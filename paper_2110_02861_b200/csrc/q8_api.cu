@@ -1,6 +1,7 @@
 // q8_api.cu -- the C ABI declared in include/q8.h: validation, host scalars, per-device
 // table cache and kernel launches.  No compute happens on the host except the once-per-
 // process codebook/threshold construction (a1) and the per-call fp32 scalars (G8-G10).
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -11,6 +12,9 @@
 
 #include "../../include/q8.h"
 #include "q8_kernels.cuh"
+#include "q8_codec.cuh"
+#include "q8_launch.h"
+#include "q8_step_kernel.cuh"
 
 namespace q8 {
 void build_dynamic_codebook(bool is_signed, float out[256]);
@@ -157,9 +161,10 @@ q8_status validate_tensor(q8_kind kind, q8_dtype gdt, const q8_tensor& t, int id
     if (!t.p || !t.g || !t.s1 || !t.absmax1 || (two && (!t.s2 || !t.absmax2)))
         return fail(Q8_ERR_INVALID, "tensor %d: NULL buffer with n > 0", idx);
     if (!aligned(t.p, 16)) return fail(Q8_ERR_INVALID, "tensor %d: p not 16-byte aligned", idx);
-    if (!aligned(t.g, gdt == Q8_F32 ? 16 : 8)) return fail(Q8_ERR_INVALID, "tensor %d: g misaligned", idx);
-    if (!aligned(t.s1, 4) || (two && !aligned(t.s2, 4)))
-        return fail(Q8_ERR_INVALID, "tensor %d: codes not 4-byte aligned", idx);
+    // 16 B: the step kernel moves each full block with TMA bulk copies (16-byte granules)
+    if (!aligned(t.g, 16)) return fail(Q8_ERR_INVALID, "tensor %d: g not 16-byte aligned", idx);
+    if (!aligned(t.s1, 16) || (two && !aligned(t.s2, 16)))
+        return fail(Q8_ERR_INVALID, "tensor %d: codes not 16-byte aligned", idx);
     if (!aligned(t.absmax1, 4) || (two && !aligned(t.absmax2, 4)))
         return fail(Q8_ERR_INVALID, "tensor %d: absmax not 4-byte aligned", idx);
     return Q8_OK;
@@ -174,33 +179,34 @@ int search_variant() {
     return v;
 }
 
-template <int KIND, int GDT, int MAXT, int SEARCH>
-q8_status launch_step_v(const q8::StepParams<MAXT>& P, const DeviceState* d, cudaStream_t st) {
-    auto fn = q8::optim8bit_step_kernel<KIND, GDT, MAXT, SEARCH>;
-    static int occ = ctas_per_sm(reinterpret_cast<const void*>(fn));
-    const int64_t grid = grid_for(d, occ, P.total_blocks);
-    fn<<<static_cast<unsigned>(grid), q8::kThreads, 0, st>>>(P, d->tabs);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e, "optim8bit_step_kernel launch");
-    return Q8_OK;
+// Sub-blocks (256-thread groups, one 2048-element block each) per persistent CTA.
+int nsub_variant() {
+    static const int v = [] {
+        const char* env = std::getenv("Q8_NSUB");
+        const int n = env ? std::atoi(env) : 3;
+        return (n == 2 || n == 3 || n == 4) ? n : 3;
+    }();
+    return v;
 }
 
-template <int KIND, int GDT, int MAXT>
-q8_status launch_step(const q8::StepParams<MAXT>& P, const DeviceState* d, cudaStream_t st) {
-    if (search_variant() == q8::SEARCH_EYTZINGER) return launch_step_v<KIND, GDT, MAXT, q8::SEARCH_EYTZINGER>(P, d, st);
-    return launch_step_v<KIND, GDT, MAXT, q8::SEARCH_BUCKET>(P, d, st);
-}
+std::mutex g_smem_mu;
+const void* g_smem_done[256];
 
 template <int MAXT>
 q8_status dispatch_step(q8_kind kind, q8_dtype gdt, const q8::StepParams<MAXT>& P, const DeviceState* d,
                         cudaStream_t st) {
-#define Q8_CASE(K, G) \
-    if (kind == K && gdt == G) return launch_step<K, G, MAXT>(P, d, st);
-    Q8_CASE(Q8_ADAM, Q8_F32) Q8_CASE(Q8_ADAM, Q8_F16) Q8_CASE(Q8_ADAM, Q8_BF16)
-    Q8_CASE(Q8_ADAMW, Q8_F32) Q8_CASE(Q8_ADAMW, Q8_F16) Q8_CASE(Q8_ADAMW, Q8_BF16)
-    Q8_CASE(Q8_MOMENTUM, Q8_F32) Q8_CASE(Q8_MOMENTUM, Q8_F16) Q8_CASE(Q8_MOMENTUM, Q8_BF16)
-#undef Q8_CASE
-    return fail(Q8_ERR_INVALID, "bad kind/dtype");
+    const q8::LaunchCtx ctx{d->tabs, d->sms, st, search_variant(), nsub_variant()};
+    const q8::StepParams<1>* single = nullptr;
+    const q8::StepParams<q8::kMultiMaxT>* multi = nullptr;
+    if constexpr (MAXT == 1) single = &P; else multi = &P;
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (gdt) {
+        case Q8_F32: e = q8::launch_step_g0(kind, single, multi, ctx); break;
+        case Q8_F16: e = q8::launch_step_g1(kind, single, multi, ctx); break;
+        case Q8_BF16: e = q8::launch_step_g2(kind, single, multi, ctx); break;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "optim8bit_step_kernel launch");
+    return Q8_OK;
 }
 
 q8_status check_common(q8_dtype gdt, int32_t blocksize) {
@@ -211,6 +217,17 @@ q8_status check_common(q8_dtype gdt, int32_t blocksize) {
 }
 
 }  // namespace
+
+cudaError_t q8::ensure_smem(const void* fn, int smem) {
+    std::lock_guard<std::mutex> lock(g_smem_mu);
+    for (const void* c : g_smem_done)
+        if (c == fn) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    for (auto& c : g_smem_done)
+        if (!c) { c = fn; break; }
+    return cudaSuccess;
+}
 
 extern "C" {
 
@@ -255,18 +272,19 @@ q8_status q8_quantize_blockwise_dynamic(int32_t is_signed, const float* x_dev, f
     if (q8_status s = device_state(&d); s != Q8_OK) return s;
     const int64_t nb = (n + q8::kBlock - 1) / q8::kBlock;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (is_signed) {
-        static int occ = ctas_per_sm(reinterpret_cast<const void*>(q8::quantize_blockwise_dynamic_kernel<true>));
-        q8::quantize_blockwise_dynamic_kernel<true>
-            <<<static_cast<unsigned>(grid_for(d, occ, nb)), q8::kThreads, 0, st>>>(d->tabs, x_dev, absmax_dev,
-                                                                                   codes_dev, n, nb);
-    } else {
-        static int occ = ctas_per_sm(reinterpret_cast<const void*>(q8::quantize_blockwise_dynamic_kernel<false>));
-        q8::quantize_blockwise_dynamic_kernel<false>
-            <<<static_cast<unsigned>(grid_for(d, occ, nb)), q8::kThreads, 0, st>>>(d->tabs, x_dev, absmax_dev,
-                                                                                   codes_dev, n, nb);
-    }
-    cudaError_t e = cudaGetLastError();
+    const void* fn = is_signed ? reinterpret_cast<const void*>(q8::quantize_blockwise_dynamic_kernel<true, 3>)
+                               : reinterpret_cast<const void*>(q8::quantize_blockwise_dynamic_kernel<false, 3>);
+    const int smem = q8::step_smem_bytes(3);
+    cudaError_t e = q8::ensure_smem(fn, smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((nb + 2) / 3, d->sms));
+    if (is_signed)
+        q8::quantize_blockwise_dynamic_kernel<true, 3><<<grid, 3 * q8::kSubThreads, smem, st>>>(d->tabs, x_dev,
+                                                                                             absmax_dev, codes_dev, n, nb);
+    else
+        q8::quantize_blockwise_dynamic_kernel<false, 3><<<grid, 3 * q8::kSubThreads, smem, st>>>(d->tabs, x_dev,
+                                                                                              absmax_dev, codes_dev, n, nb);
+    e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "quantize_blockwise_dynamic_kernel launch");
     return ok();
 }

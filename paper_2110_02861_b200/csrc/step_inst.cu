@@ -1,0 +1,59 @@
+// step_inst.cu -- instantiates and launches the fused step kernels for ONE gradient dtype
+// (Q8_GDT = 0 fp32, 1 fp16, 2 bf16); build.py compiles this file once per dtype in parallel.
+#include "q8_launch.h"
+#include "q8_step_kernel.cuh"
+
+#ifndef Q8_GDT
+#error "compile with -DQ8_GDT=0|1|2"
+#endif
+
+namespace q8 {
+namespace {
+
+template <typename Kern, typename... Args>
+cudaError_t persistent(Kern fn, int nsub, int64_t work_blocks, const LaunchCtx& ctx, const Args&... args) {
+    const int smem = step_smem_bytes_tma(nsub, Q8_GDT);
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
+    if (e != cudaSuccess) return e;
+    int64_t grid = (work_blocks + nsub - 1) / nsub;
+    if (grid > ctx.sms) grid = ctx.sms;
+    fn<<<static_cast<unsigned>(grid), nsub * kSubThreads, smem, ctx.stream>>>(args...);
+    return cudaGetLastError();
+}
+
+template <int KIND, int MAXT>
+cudaError_t launch_kind(const StepParams<MAXT>& P, const LaunchCtx& ctx) {
+    constexpr int G = Q8_GDT;
+    if (ctx.search == SEARCH_EYTZINGER)  // reference variant: one configuration
+        return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_EYTZINGER, 3>, 3, P.total_blocks, ctx, P,
+                          ctx.tabs);
+    switch (ctx.nsub) {
+        case 2: return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, 2>, 2, P.total_blocks, ctx, P,
+                                  ctx.tabs);
+        case 4: return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, 4>, 4, P.total_blocks, ctx, P,
+                                  ctx.tabs);
+        default: return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, 3>, 3, P.total_blocks, ctx, P,
+                                   ctx.tabs);
+    }
+}
+
+template <int MAXT>
+cudaError_t launch_any(int kind, const StepParams<MAXT>& P, const LaunchCtx& ctx) {
+    switch (kind) {
+        case KIND_ADAM: return launch_kind<KIND_ADAM, MAXT>(P, ctx);
+        case KIND_ADAMW: return launch_kind<KIND_ADAMW, MAXT>(P, ctx);
+        case KIND_MOMENTUM: return launch_kind<KIND_MOMENTUM, MAXT>(P, ctx);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace
+
+#define Q8_CAT2(a, b) a##b
+#define Q8_CAT(a, b) Q8_CAT2(a, b)
+cudaError_t Q8_CAT(launch_step_g, Q8_GDT)(int kind, const StepParams<1>* single,
+                                          const StepParams<kMultiMaxT>* multi, const LaunchCtx& ctx) {
+    return single ? launch_any<1>(kind, *single, ctx) : launch_any<kMultiMaxT>(kind, *multi, ctx);
+}
+
+}  // namespace q8
