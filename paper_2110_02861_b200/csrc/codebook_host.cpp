@@ -82,28 +82,28 @@ static int code_of(const float T[256], float y) {
     return c;
 }
 
-// Bucket tables of the bucketed search (q8_kernels.cuh "Bucketed search").  Bucket mk covers
-// the fp32 magnitudes whose bits lie in [(mk + base) << shift, (mk + base + 1) << shift),
-// where base = bits(2^-22) >> shift, clamped to [0, 1]; bucket 0 also holds every magnitude
-// below 2^-22.  lut[key] = smallest code in the bucket.  Returns false if some bucket spans
-// more than two codes (then the one-compare finish would be wrong).
-bool build_bucket_lut(const float T[256], bool is_signed, uint32_t min_mag_bits, int shift, int nbuckets,
-                      int neg_offset, uint8_t* lut, int lut_bytes) {
-    std::memset(lut, 0, static_cast<size_t>(lut_bytes));
-    const uint32_t base = min_mag_bits >> shift;
-    for (int mk = 0; mk < nbuckets; ++mk) {
-        uint32_t lo = (mk == 0) ? 0u : ((base + static_cast<uint32_t>(mk)) << shift);
-        uint32_t hi = ((base + static_cast<uint32_t>(mk) + 1u) << shift) - 1u;
-        if (hi > 0x3f800000u) hi = 0x3f800000u;
-        const float flo = bits_to_float(lo), fhi = bits_to_float(hi);
-        int c_lo = code_of(T, flo), c_hi = code_of(T, fhi);
-        if (c_hi - c_lo > 1 || mk >= lut_bytes) return false;
-        lut[mk] = static_cast<uint8_t>(c_lo);
-        if (is_signed) {
-            const int c_nlo = code_of(T, -fhi), c_nhi = code_of(T, -flo);
-            if (c_nhi - c_nlo > 1 || neg_offset + mk >= lut_bytes) return false;
-            lut[neg_offset + mk] = static_cast<uint8_t>(c_nlo);
+// Bucket tables of the bucketed search (q8_kernels.cuh "Bucketed search").  Key k covers the
+// fp32 bit patterns [k << shift, (k + 1) << shift) (signed: sign bit included in the key).
+// lut[k] = smallest code of any value in [-1, 1] (signed) / [0, 1] (unsigned) in the bucket;
+// keys beyond that range are unreachable for a normalized value and hold 255 (positive) or 0
+// (negative).  Returns false if some bucket spans more than two codes.
+bool build_bucket_lut(const float T[256], bool is_signed, int shift, int entries, uint8_t* lut) {
+    const uint32_t one = 0x3f800000u, width = 1u << shift;
+    for (int k = 0; k < entries; ++k) {
+        const uint32_t hi_bits = static_cast<uint32_t>(k) << shift;
+        const bool neg = is_signed && (hi_bits & 0x80000000u);
+        const uint32_t mlo = hi_bits & 0x7fffffffu;
+        if (mlo > one) {                       // |y| > 1: unreachable
+            lut[k] = neg ? 0 : 255;
+            continue;
         }
+        uint32_t mhi = mlo + width - 1u;
+        if (mhi > one) mhi = one;
+        const float a = bits_to_float(mlo), b = bits_to_float(mhi);
+        const float lo = neg ? -b : a, hi = neg ? -a : b;   // the bucket's value range
+        const int c_lo = code_of(T, lo), c_hi = code_of(T, hi);
+        if (c_hi - c_lo > 1) return false;
+        lut[k] = static_cast<uint8_t>(c_lo);
     }
     return true;
 }

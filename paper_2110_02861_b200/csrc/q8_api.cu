@@ -20,8 +20,7 @@ namespace q8 {
 void build_dynamic_codebook(bool is_signed, float out[256]);
 void build_eytzinger_thresholds(const float Q[256], float out[256]);
 void build_sorted_thresholds(const float Q[256], float out[256]);
-bool build_bucket_lut(const float T[256], bool is_signed, uint32_t min_mag_bits, int shift, int nbuckets,
-                      int neg_offset, uint8_t* lut, int lut_bytes);
+bool build_bucket_lut(const float T[256], bool is_signed, int shift, int entries, uint8_t* lut);
 }  // namespace q8
 
 namespace {
@@ -74,10 +73,8 @@ q8_status device_state(DeviceState** out) {
         q8::build_eytzinger_thresholds(host + q8::kTabQu, host + q8::kTabTu);
         q8::build_sorted_thresholds(host + q8::kTabQu, host + q8::kTabSu);
         uint8_t* lut = reinterpret_cast<uint8_t*>(host + q8::kTabLut);
-        if (!q8::build_bucket_lut(host + q8::kTabSs, true, q8::kMinMagBits, q8::kShiftS, q8::kBucketsS, q8::kNegOffS,
-                                  lut, q8::kLutSBytes) ||
-            !q8::build_bucket_lut(host + q8::kTabSu, false, q8::kMinMagBits, q8::kShiftU, q8::kBucketsU, 0,
-                                  lut + q8::kLutSBytes, q8::kLutUBytes))
+        if (!q8::build_bucket_lut(host + q8::kTabSs, true, q8::kShiftS, q8::kLutSBytes, lut) ||
+            !q8::build_bucket_lut(host + q8::kTabSu, false, q8::kShiftU, q8::kLutUBytes, lut + q8::kLutSBytes))
             return fail(Q8_ERR_CUDA, "internal: bucket table spans more than two codes");
         float* ptr = nullptr;
         e = cudaMalloc(&ptr, sizeof host);
@@ -151,6 +148,7 @@ q8::StepScalars make_scalars(const q8_hparams* hp, int64_t step) {
     }
     s.wd = static_cast<float>(hp->weight_decay);
     s.decay = static_cast<float>(1.0 - hp->lr * hp->weight_decay);
+    s.fast_div = (s.eps_hat >= 0x1p-40f && std::isfinite(s.eps_hat)) ? 1 : 0;
     return s;
 }
 
@@ -274,7 +272,7 @@ q8_status q8_quantize_blockwise_dynamic(int32_t is_signed, const float* x_dev, f
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const void* fn = is_signed ? reinterpret_cast<const void*>(q8::quantize_blockwise_dynamic_kernel<true, 3>)
                                : reinterpret_cast<const void*>(q8::quantize_blockwise_dynamic_kernel<false, 3>);
-    const int smem = q8::step_smem_bytes(3);
+    const int smem = q8::step_smem_bytes(1, q8::G_F32);
     cudaError_t e = q8::ensure_smem(fn, smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((nb + 2) / 3, d->sms));

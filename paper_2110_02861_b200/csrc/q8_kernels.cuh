@@ -41,19 +41,13 @@ constexpr int kTabQs = 0, kTabTs = 256, kTabQu = 512, kTabTu = 768, kTabSs = 102
 constexpr int kTabLut = 1536;                     // word offset of the byte tables
 
 // Bucketed search.  The binary search's first seven levels are replaced by
-// one table lookup indexed by the leading bits of y, the eighth by a compare:
-//   signed:   mag = |y| bits clamped below at 2^-22;  mk = (mag >> 17) - (2^-22 bits >> 17)
-//             (exponent + 6 mantissa bits, 1409 buckets over [0, 1]); key = mk + 1536*[y < 0]
-//   unsigned: mk = (max(bits, 2^-22 bits) >> 16) - (2^-22 bits >> 16)  (7 mantissa bits, 2817)
-// LUT[key] = c0 = the smallest code in the bucket.  Every bucket spans at most two codes
-// (verified exhaustively at table-build time), so code = c0 + [y > T_{c0}]  (T sorted).
-constexpr uint32_t kMinMagBits = (127u - 22u) << 23;   // 2^-22: below every |threshold| (>= 1.6e-7)
+// one lookup in a table indexed directly by the leading bits of y, the eighth by a compare:
+//   signed:   key = bits(y) >> 17  (sign, exponent, 6 mantissa bits); 0x6000 keys cover [-1, 1]
+//   unsigned: key = bits(y) >> 16  (exponent, 7 mantissa bits);       0x4000 keys cover [0, 1]
+// LUT[key] = c0 = the smallest code of any y in the bucket.  Every bucket spans at most two
+// codes (checked exhaustively when the tables are built), so code = c0 + [y > T_{c0}].
 constexpr int kShiftS = 17, kShiftU = 16;
-constexpr int kBucketsS = ((0x3f800000 >> kShiftS) - (kMinMagBits >> kShiftS)) + 1;  // 1409
-constexpr int kBucketsU = ((0x3f800000 >> kShiftU) - (kMinMagBits >> kShiftU)) + 1;  // 2817
-constexpr int kNegOffS = 1536;
-constexpr int kLutSBytes = 3072;                   // [0,1409) y >= 0, [1536, 2945) y < 0
-constexpr int kLutUBytes = 2944;                   // 2817 used, padded to a multiple of 128
+constexpr int kLutSBytes = 0x6000, kLutUBytes = 0x4000;
 constexpr int kTabBytes = kTabLut * 4 + kLutSBytes + kLutUBytes;
 constexpr int kTabFloats = kTabBytes / 4;
 constexpr int SEARCH_EYTZINGER = 0, SEARCH_BUCKET = 1;
@@ -70,6 +64,7 @@ struct TensorDesc {
 
 struct StepScalars {       // all computed on the host in double, rounded once (G8-G10)
     float lr, beta1, beta2, omb1, omb2, step_size, eps_hat, wd, decay;
+    int fast_div;          // eps_hat >= 2^-40: the packed sqrt/div fast path may be used
 };
 
 template <int MAXT>

@@ -12,7 +12,7 @@ namespace {
 
 template <typename Kern, typename... Args>
 cudaError_t persistent(Kern fn, int nsub, int64_t work_blocks, const LaunchCtx& ctx, const Args&... args) {
-    const int smem = step_smem_bytes_tma(nsub, Q8_GDT);
+    const int smem = step_smem_bytes(nsub, Q8_GDT);
     cudaError_t e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
     if (e != cudaSuccess) return e;
     int64_t grid = (work_blocks + nsub - 1) / nsub;
