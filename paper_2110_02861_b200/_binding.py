@@ -9,7 +9,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libq8.so")
+# Q8_LIB_PATH: development A/B override of the library file (tools/probe_step.py)
+LIB_PATH = os.environ.get("Q8_LIB_PATH") or os.path.join(_HERE, "libq8.so")
 
 Q8_OK, Q8_ERR_INVALID, Q8_ERR_UNSUPPORTED, Q8_ERR_CUDA = 0, -1, -2, -3
 Q8_F32, Q8_F16, Q8_BF16 = 0, 1, 2
