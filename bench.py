@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the fused block-wise 8-bit optimizer step (Dettmers et al. 2021,
+arXiv 2110.02861) on B200, BASELINE.json's metric: parameters updated per second and achieved
+HBM GB/s against the measured peak.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
+
+Workload (default): BASELINE config 4 -- 8-bit AdamW over a 1,557,611,200-parameter
+GPT-2-XL-shaped flat fp32 buffer with bf16 gradients, blocksize 2048.  With N > 1 (torchrun,
+one process per GPU, NCCL) the buffer is ZeRO-1 sharded on block boundaries: each rank steps
+its own 1/N (strong scaling); ``value`` = all parameters / max-over-ranks step time.  The
+ZeRO-1 reduce-scatter -> step -> all-gather round trip is timed separately under "zero1".
+
+A "step" is one launch of the fused kernel over the whole (shard) buffer: dequantize, fp32
+AdamW update, block absmax, requantize.  Inputs (21.8 GB per step)
+exceed the 126 MB L2, so no flush is needed between steps.  ``--impl reference`` times the
+CPU oracle (oracle/) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "8-bit Adam params updated/sec and achieved HBM GB/s vs peak, 1/2/4/8 B200"
+UNIT = "params/s"
+TORCH_DT = {"float32": torch.float32, "float16": torch.float16, "bfloat16": torch.bfloat16}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="cfg4_gpt2_xl")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--zero1-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def bytes_per_param(kind: str, grad_dtype: str) -> float:
+    """Algorithmic HBM bytes per parameter per step: p read+write 8, g 2|4,
+    codes read+write 2 per state, absmax read+write 8 B per 2048-block per state."""
+    states = 1 if kind == "momentum" else 2
+    return 8 + (4 if grad_dtype == "float32" else 2) + 2 * states + 8 * states / 2048
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def workload_config(name, world):
+    w = synth.WORKLOADS[name]
+    n = synth.workload_numel(name)
+    return dict(workload=f"{name}: {w['desc']}", n_params=n, kind=w["kind"], grad_dtype=w["grad_dtype"],
+                state="uint8 codes + fp32 absmax per 2048-block (signed dynamic tree s1, unsigned dynamic s2)",
+                blocksize=2048, hparams=synth.HPARAMS[w["kind"]],
+                parallelism=f"zero1-dp{world}" if world > 1 else "single-gpu",
+                l2="inputs of one step exceed the 126 MB L2; no flush between steps")
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.gpu), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+
+def oracle_sample(cfg, target_s: float = 10.0):
+    """Time the CPU oracle (as it stands) on a bounded slice of the workload; returns
+    (params/s, cores, sample description).  Blocks are independent, so a slice of
+    whole blocks is a faithful sample of the per-parameter work."""
+    import numpy as np
+
+    import oracle
+    cores = os.cpu_count() or 1
+    kind, gdt = cfg["kind"], cfg["grad_dtype"]
+    hp = dict(cfg["hparams"])
+
+    def run(n):
+        p = synth.params(n, seed=11).numpy()
+        g = synth.to_f32_numpy(synth.grads(n, step=3, seed=11, dtype=gdt))
+        s1, a1 = (t.numpy() for t in synth.random_state(n, seed=12, scale=1e-3))
+        s2, a2 = (t.numpy() for t in synth.random_state(n, seed=13, scale=1e-6))
+        t0 = time.perf_counter()
+        oracle.optim8bit_step(kind, p, g, s1, s2, a1, a2, step=3, nthreads=cores, **hp)
+        return time.perf_counter() - t0, np
+
+    n = 1 << 21
+    dt, _ = run(n)
+    n2 = int(min(cfg["n_params"], max(n, n * target_s / max(dt, 1e-3))))
+    n2 = max(2048, n2 // 2048 * 2048)
+    dt2, _ = run(n2)
+    return n2 / dt2, cores, (f"{n2:,} parameters ({n2 // 2048:,} whole blocks) of {cfg['workload'].split(':')[0]}, "
+                             f"one {kind} step, {cores} threads, {dt2:.1f} s")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if rank != 0:
+        return
+    cfg = workload_config(args.workload, world)
+    import oracle
+    cores = os.cpu_count() or 1
+    kind, gdt = cfg["kind"], cfg["grad_dtype"]
+    # each step is a bounded sample sized so the whole run stays within a few minutes
+    n = 1 << 22
+    p = synth.params(n, seed=11).numpy()
+    s1, a1 = (t.numpy() for t in synth.zero_state(n))
+    s2, a2 = (t.numpy() for t in synth.zero_state(n))
+    gs = [synth.to_f32_numpy(synth.grads(n, step=t, seed=11, dtype=gdt)) for t in (1, 2)]
+    hp = dict(cfg["hparams"])
+    t = 0
+    for _ in range(args.warmup):
+        t += 1
+        oracle.optim8bit_step(kind, p, gs[t % 2], s1, s2, a1, a2, step=t, nthreads=cores, **hp)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        t += 1
+        oracle.optim8bit_step(kind, p, gs[t % 2], s1, s2, a1, a2, step=t, nthreads=cores, **hp)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = n / dt
+    sample = f"{n:,} parameters ({n // 2048:,} blocks) of {args.workload} per step, {cores} threads"
+    print(json.dumps({
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference", "config": cfg,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ----------------------------------------------------------------------------- GPU
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import paper_2110_02861_b200 as q8
+    from paper_2110_02861_b200 import zero
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = workload_config(args.workload, world)
+    kind, gdt = cfg["kind"], cfg["grad_dtype"]
+    hp = dict(cfg["hparams"])
+    n_total = cfg["n_params"]
+    n_pad = zero.padded_numel(n_total, world)
+    lo, hi = zero.shard_range(n_pad, world, rank)
+    shard = hi - lo
+    valid = max(0, min(hi, n_total) - lo)  # real (non-padding) parameters of this shard
+
+    # ---- device-resident shard state (the timed step touches only HBM)
+    p = synth.params(shard, seed=1 + rank, device=dev)
+    if valid < shard:
+        p[valid:].zero_()
+    gpool = []
+    for t in (1, 2):
+        g = synth.grads(shard, step=t, seed=rank, dtype=gdt, device=dev)
+        if valid < shard:
+            g[valid:].zero_()
+        gpool.append(g)
+    s1, a1 = synth.zero_state(shard, device=dev)
+    s2, a2 = synth.zero_state(shard, device=dev)
+    hpo = q8.hparams(**hp)
+    step = 0
+
+    def one(stream_g):
+        nonlocal step
+        step += 1
+        q8.optim8bit_step(kind, p, stream_g, s1, s2, a1, a2, step=step, hp=hpo, lr=hp["lr"])
+
+    for i in range(args.warmup):
+        one(gpool[i % 2])
+    torch.cuda.synchronize()
+    # state realism check: the most common code should hold < 5% of elements
+    share1 = float(torch.bincount(s1[:1 << 24].to(torch.int64), minlength=256).max()) / min(shard, 1 << 24)
+
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            one(gpool[i % 2])
+            ev[i][1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    ms_local = torch.tensor([total_ms / args.steps, kern_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_local, op=dist.ReduceOp.MAX)
+    ms_per_step, kern_ms_max = float(ms_local[0]), float(ms_local[1])
+    value = n_total / (ms_per_step / 1e3)
+
+    peaks = measured_peaks()
+    bpp = bytes_per_param(kind, gdt)
+    achieved = shard * bpp / (kern_ms / 1e3) / 1e9
+    peak = peaks.get("hbm_gbs", 6650.0)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if world == 1 and os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "algorithmic_bytes_per_launch": shard * bpp,
+                "bytes_per_param": bpp, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+                if "hbm_gbs" in peaks else "fallback 6.65 TB/s (B200_PROFILING.md)",
+                "frac_of_8TBs_spec": achieved / 8000.0, "kernel": "optim8bit_step_kernel",
+                "kernel_ms": kern_ms_max}
+
+    # ---- end to end through the public API with host buffers: per step the bf16 gradients
+    #      arrive from pinned host memory and the updated fp32 parameters go back to the host
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        g_host = torch.empty(shard, dtype=TORCH_DT[gdt]).pin_memory()
+        g_host.copy_(gpool[0])
+        p_host = torch.empty(shard, dtype=torch.float32).pin_memory()
+        g_dev = torch.empty(shard, dtype=TORCH_DT[gdt], device=dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.e2e_steps):
+            g_dev.copy_(g_host, non_blocking=True)
+            one(g_dev)
+            p_host.copy_(p, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        em = torch.tensor([a.elapsed_time(b) / args.e2e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(em, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_total / (float(em[0]) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": n_pad * g_host.element_size(), "d2h_bytes_per_step": n_pad * 4,
+               "ms_per_step": float(em[0]), "path": "pinned host bf16 grads -> H2D -> q8_optim8bit_step -> D2H fp32 params"}
+
+    # ---- ZeRO-1 round trip (N > 1): reduce-scatter bf16 grads -> shard step -> all-gather params
+    zero1 = None
+    if world > 1 and args.zero1_steps > 0:
+        del gpool
+        torch.cuda.empty_cache()
+        zo = zero.Zero1Optimizer8bit(n_total, kind=kind, grad_dtype=TORCH_DT[gdt], device=dev, **hp)
+        zo.params[:n_total].normal_(0, 0.02)
+        zo.grads[:n_total].normal_(0, 1e-3)
+        for _ in range(2):
+            zo.step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        rs = st = ag = 0.0
+        for _ in range(args.zero1_steps):
+            e[0].record()
+            zo.reduce_scatter()
+            e[1].record()
+            zo.shard_step()
+            e[2].record()
+            zo.all_gather()
+            e[3].record()
+            torch.cuda.synchronize()
+            rs += e[0].elapsed_time(e[1])
+            st += e[1].elapsed_time(e[2])
+            ag += e[2].elapsed_time(e[3])
+        zt = torch.tensor([rs, st, ag], dtype=torch.float64, device=dev) / args.zero1_steps
+        dist.all_reduce(zt, op=dist.ReduceOp.MAX)
+        tot = float(zt.sum())
+        zero1 = {"ms_per_step": tot, "params_per_s": n_total / (tot / 1e3), "reduce_scatter_ms": float(zt[0]),
+                 "shard_step_ms": float(zt[1]), "all_gather_ms": float(zt[2]),
+                 "reduce_scatter_bytes_per_rank": n_pad * (2 if gdt != "float32" else 4),
+                 "all_gather_bytes_per_rank": n_pad * 4, "backend": "nccl", "steps": args.zero1_steps}
+        del zo
+        torch.cuda.empty_cache()
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, cores, sample = oracle_sample(cfg)
+        cpu_baseline = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: p~N(0,0.02^2), bf16 g~N(0,1e-3^2) (pool of 2), 8-bit states evolved from zero "
+                    f"over the warm-up; most common s1 code after warm-up holds {100 * share1:.1f}% of elements",
+            "config": cfg, "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "zero1": zero1,
+            "gpu_launches": args.steps, "clocks": clk.summary(),
+            "achieved_gbs_whole_job": n_total * bpp / (ms_per_step / 1e3) / 1e9,
+            "library": q8.version(),
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -14,3 +14,8 @@ __all__ = [
     "dequantize_blockwise", "hparams", "nblocks", "optim8bit_step", "optim8bit_step_multi", "quantize_blockwise",
     "quantize_blockwise_dynamic", "version",
 ]
+from .optim import Adam8bit, AdamW8bit, Momentum8bit, state_bytes  # noqa: E402
+from .zero import Zero1Optimizer8bit, padded_numel, shard_range  # noqa: E402
+
+__all__ += ["Adam8bit", "AdamW8bit", "Momentum8bit", "state_bytes", "Zero1Optimizer8bit", "padded_numel",
+            "shard_range"]

@@ -1,0 +1,100 @@
+"""torch.optim-style 8-bit optimizers over the fused sm_100a step (the paper's "two-line
+change", P:7 / P:28: swap the optimizer class).
+
+Each parameter keeps its optimizer state as 8-bit codes plus one fp32 absmax per 2048-element
+block (S3.1): ``s1``/``absmax1`` for the first state (signed dynamic tree type),
+``s2``/``absmax2`` for Adam's second state (unsigned dynamic type).  A step groups all
+parameters that have gradients by gradient dtype and calls ``q8_optim8bit_step_multi`` once
+per group (one kernel launch per <= 384 tensors).  Parameters must be fp32, contiguous and
+16-byte aligned on a CUDA device; there is no CPU path.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _binding as B
+
+
+class _Optimizer8bit(torch.optim.Optimizer):
+    kind = "adam"
+
+    def __init__(self, params, lr=1e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.0, bias_correction=True):
+        if lr < 0 or eps <= 0 or not (0 <= betas[0] < 1) or not (0 <= betas[1] < 1) or weight_decay < 0:
+            raise ValueError("invalid hyper-parameters")
+        super().__init__(params, dict(lr=lr, betas=tuple(betas), eps=eps, weight_decay=weight_decay,
+                                      bias_correction=bias_correction))
+        self._lists = {}
+
+    def _state_for(self, p: torch.Tensor):
+        st = self.state[p]
+        if not st:
+            if p.dtype != torch.float32 or not p.is_cuda:
+                raise TypeError("8-bit optimizers update fp32 CUDA parameters")
+            n = p.numel()
+            nb = B.nblocks(n)
+            st["step"] = 0
+            st["s1"] = torch.zeros(n, dtype=torch.uint8, device=p.device)
+            st["absmax1"] = torch.zeros(nb, dtype=torch.float32, device=p.device)
+            if self.kind != "momentum":
+                st["s2"] = torch.zeros(n, dtype=torch.uint8, device=p.device)
+                st["absmax2"] = torch.zeros(nb, dtype=torch.float32, device=p.device)
+        return st
+
+    @torch.no_grad()
+    def step(self, closure=None):
+        loss = None
+        if closure is not None:
+            with torch.enable_grad():
+                loss = closure()
+        for group in self.param_groups:
+            buckets = {}
+            for p in group["params"]:
+                if p.grad is None:
+                    continue
+                if p.grad.is_sparse:
+                    raise TypeError("sparse gradients are not supported")
+                st = self._state_for(p)
+                st["step"] += 1
+                g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
+                buckets.setdefault((g.dtype, st["step"]), []).append(
+                    (p, g, st["s1"], st.get("s2"), st["absmax1"], st.get("absmax2")))
+            b1, b2 = group["betas"]
+            hp = B.hparams(group["lr"], b1, b2, group["eps"], group["weight_decay"], group["bias_correction"])
+            for (_, step), entries in buckets.items():
+                key = tuple(t.data_ptr() if t is not None else 0 for e in entries for t in e)
+                tl = self._lists.get(key)
+                if tl is None:
+                    tl = B.TensorList(entries)
+                    if len(self._lists) > 64:
+                        self._lists.clear()
+                    self._lists[key] = tl
+                B.optim8bit_step_multi(self.kind, tl, lr=group["lr"], step=step, hp=hp)
+        return loss
+
+
+class Adam8bit(_Optimizer8bit):
+    """Adam (Eq.2) with 8-bit block-wise dynamic states; L2 weight decay."""
+    kind = "adam"
+
+
+class AdamW8bit(_Optimizer8bit):
+    """AdamW: Adam with decoupled weight decay (Loshchilov & Hutter, cited P:134)."""
+    kind = "adamw"
+
+    def __init__(self, params, lr=1e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=1e-2, bias_correction=True):
+        super().__init__(params, lr, betas, eps, weight_decay, bias_correction)
+
+
+class Momentum8bit(_Optimizer8bit):
+    """SGD with momentum, Eq.1: m = beta*m + g, w -= lr*m (no dampening)."""
+    kind = "momentum"
+
+    def __init__(self, params, lr=0.1, momentum=0.9, weight_decay=0.0):
+        super().__init__(params, lr, (momentum, 0.0), 1e-8, weight_decay, False)
+
+
+def state_bytes(n_params: int, kind: str = "adam", blocksize: int = B.BLOCKSIZE) -> int:
+    """Optimizer-state bytes of the 8-bit optimizer: 1 B per element per state plus one fp32
+    absmax per block per state (8 GB -> 2 GB for a 1B-parameter Adam)."""
+    states = 1 if kind == "momentum" else 2
+    return states * (n_params + 4 * B.nblocks(n_params, blocksize))

@@ -1,0 +1,90 @@
+"""ZeRO-1 data parallelism for the 8-bit step (optimizer sharding is cited as
+complementary in the paper, P:259 S6).
+
+One process per GPU.  The flat fp32 parameter buffer is padded to a multiple of
+``world * 2048`` elements (zero padding is neutral: zeros never raise a block's absmax and
+padded p, g stay 0) and split on block boundaries, so every rank's shard is a whole number of
+2048-element blocks (blocks are independent, P:110 -- the sharded result equals the
+unsharded one bit for bit).  Each step:
+
+  1. ``reduce_scatter_tensor`` of the full gradient buffer (NCCL over NVLink; op AVG)
+  2. the fused 8-bit step on this rank's shard (its own 8-bit states only)
+  3. ``all_gather_into_tensor`` of the updated parameter shards back into the full buffer.
+
+``step_fn`` is the per-shard step; it defaults to the CUDA kernel and is injectable only
+so the collective plumbing can be tested on CPU ranks (gloo).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import _binding as B
+
+
+def padded_numel(n: int, world: int, blocksize: int = B.BLOCKSIZE) -> int:
+    unit = world * blocksize
+    return (n + unit - 1) // unit * unit
+
+
+def shard_range(n_padded: int, world: int, rank: int):
+    shard = n_padded // world
+    return rank * shard, (rank + 1) * shard
+
+
+class Zero1Optimizer8bit:
+    def __init__(self, n_params: int, kind: str = "adamw", grad_dtype=torch.bfloat16, device=None, group=None,
+                 step_fn=None, state_device=None, **hparams):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.kind = kind
+        self.n = n_params
+        self.n_pad = padded_numel(n_params, self.world)
+        self.lo, self.hi = shard_range(self.n_pad, self.world, self.rank)
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        sdev = torch.device(state_device) if state_device is not None else dev
+        self.params = torch.zeros(self.n_pad, dtype=torch.float32, device=dev)   # full replica
+        self.grads = torch.zeros(self.n_pad, dtype=grad_dtype, device=dev)       # full local grads
+        shard = self.hi - self.lo
+        self.g_shard = torch.zeros(shard, dtype=grad_dtype, device=sdev)
+        self.s1 = torch.zeros(shard, dtype=torch.uint8, device=sdev)
+        self.absmax1 = torch.zeros(shard // B.BLOCKSIZE, dtype=torch.float32, device=sdev)
+        two = kind != "momentum"
+        self.s2 = torch.zeros(shard, dtype=torch.uint8, device=sdev) if two else None
+        self.absmax2 = torch.zeros(shard // B.BLOCKSIZE, dtype=torch.float32, device=sdev) if two else None
+        self.hp = dict(hparams)
+        self.t = 0
+        self.step_fn = step_fn or self._cuda_step
+
+    @property
+    def p_shard(self) -> torch.Tensor:
+        return self.params[self.lo:self.hi]
+
+    def _cuda_step(self, p, g, s1, s2, a1, a2, step):
+        B.optim8bit_step(self.kind, p, g, s1, s2, a1, a2, step=step, **self.hp)
+
+    def reduce_scatter(self):
+        if self.world == 1:
+            self.g_shard.copy_(self.grads[self.lo:self.hi])
+            return
+        try:
+            dist.reduce_scatter_tensor(self.g_shard, self.grads, op=dist.ReduceOp.AVG, group=self.group)
+        except (RuntimeError, ValueError):  # backends without AVG reduce-scatter (gloo)
+            dist.reduce_scatter_tensor(self.g_shard, self.grads, op=dist.ReduceOp.SUM, group=self.group)
+            self.g_shard.div_(self.world)
+
+    def all_gather(self):
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.params, self.p_shard.clone() if not self.params.is_cuda else self.p_shard,
+                                        group=self.group)
+
+    def shard_step(self):
+        self.t += 1
+        self.step_fn(self.p_shard, self.g_shard, self.s1, self.s2, self.absmax1, self.absmax2, self.t)
+
+    def step(self):
+        """reduce-scatter grads -> 8-bit step on the local shard -> all-gather params."""
+        self.reduce_scatter()
+        self.shard_step()
+        self.all_gather()

@@ -4,7 +4,7 @@ import io
 import subprocess
 import sys
 
-KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "dram__bytes_read.sum", "dram__bytes_write.sum",
+KEYS = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "sm__cycles_elapsed.avg.per_second", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "dram__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed.sum", "smsp__warps_active.avg.per_cycle_active", "smsp__warps_eligible.avg.per_cycle_active",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
@@ -26,7 +26,7 @@ def main(path, n=None):
             if k in d:
                 print(f"  {k:70s} {d[k]}")
         if n:
-            inst = float(d["sm__inst_executed.sum"].replace(",", ""))
+            inst = float((d.get("sm__inst_executed.sum") or d["smsp__inst_executed.sum"]).replace(",", ""))
             print(f"  thread-instructions per element: {inst * 32 / n:.1f}")
             sh = float(d["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"].replace(",", ""))
             print(f"  shared wavefronts per 32 elements: {sh * 32 / n:.1f}")
