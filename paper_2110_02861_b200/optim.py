@@ -40,6 +40,20 @@ class _Optimizer8bit(torch.optim.Optimizer):
                 st["absmax2"] = torch.zeros(nb, dtype=torch.float32, device=p.device)
         return st
 
+    def load_state_dict(self, state_dict):
+        # torch casts floating-point-param state to the param dtype; codes must stay uint8
+        super().load_state_dict(state_dict)
+        for st in self.state.values():
+            for k in ("s1", "s2"):
+                if k in st:
+                    st[k] = st[k].to(torch.uint8).contiguous()
+            for k in ("absmax1", "absmax2"):
+                if k in st:
+                    st[k] = st[k].to(torch.float32).contiguous()
+            if "step" in st:
+                st["step"] = int(st["step"])
+        self._lists.clear()
+
     @torch.no_grad()
     def step(self, closure=None):
         loss = None

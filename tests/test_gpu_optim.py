@@ -1,0 +1,103 @@
+"""GPU tests of the torch-facing API (the paper's "two-line change", P:7): Adam8bit / AdamW8bit /
+Momentum8bit over real nn.Module parameters equal per-tensor oracle steps bit for bit; state_dict
+save/load resumes bit-identically; ZeRO-1 with one rank equals the plain step."""
+import copy
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module")
+def q8():
+    import paper_2110_02861_b200 as m
+    return m
+
+
+def make_model():
+    torch.manual_seed(0)
+    return torch.nn.Sequential(torch.nn.Linear(300, 700), torch.nn.LayerNorm(700), torch.nn.Linear(700, 50)).to(DEV)
+
+
+@pytest.mark.parametrize("cls,kind,extra", [("Adam8bit", "adam", {}), ("AdamW8bit", "adamw", {}),
+                                            ("Momentum8bit", "momentum", {})])
+def test_optimizer_matches_oracle(q8, cls, kind, extra):
+    model = make_model()
+    ref = [p.detach().cpu().numpy().copy() for p in model.parameters()]
+    if kind == "momentum":
+        opt = q8.Momentum8bit(model.parameters(), lr=0.05, momentum=0.9, weight_decay=1e-4)
+        hp = dict(lr=0.05, beta1=0.9, beta2=0.0, eps=1e-8, weight_decay=1e-4, bias_correction=False)
+    else:
+        opt = getattr(q8, cls)(model.parameters(), lr=1e-3, betas=(0.9, 0.995), eps=1e-7, weight_decay=0.01)
+        hp = dict(lr=1e-3, beta1=0.9, beta2=0.995, eps=1e-7, weight_decay=0.01, bias_correction=True)
+    st = [dict(s1=np.zeros(p.size, np.uint8), s2=np.zeros(p.size, np.uint8),
+               a1=np.zeros((p.size + 2047) // 2048, np.float32), a2=np.zeros((p.size + 2047) // 2048, np.float32))
+          for p in ref]
+    x = torch.randn(64, 300, device=DEV)
+    for t in range(1, 4):
+        opt.zero_grad()
+        model(x).square().mean().backward()
+        grads = [p.grad.detach().cpu().numpy().copy() for p in model.parameters()]
+        opt.step()
+        for r, g, s in zip(ref, grads, st):
+            oracle.optim8bit_step(kind, r.reshape(-1), g.reshape(-1), s["s1"], s["s2"], s["a1"], s["a2"], step=t, **hp)
+        for p, r in zip(model.parameters(), ref):
+            assert np.array_equal(p.detach().cpu().numpy().view(np.uint32), r.view(np.uint32))
+
+
+def test_state_dict_resume_is_bit_identical(q8):
+    m1 = make_model()
+    m2 = copy.deepcopy(m1)
+    o1 = q8.AdamW8bit(m1.parameters(), lr=2e-3)
+    o2 = q8.AdamW8bit(m2.parameters(), lr=2e-3)
+    x = torch.randn(32, 300, device=DEV)
+
+    def step(m, o):
+        o.zero_grad()
+        m(x).square().mean().backward()
+        o.step()
+
+    for _ in range(3):
+        step(m1, o1)
+        step(m2, o2)
+    sd = copy.deepcopy(o2.state_dict())
+    msd = copy.deepcopy(m2.state_dict())
+    m3 = make_model()
+    m3.load_state_dict(msd)
+    o3 = q8.AdamW8bit(m3.parameters(), lr=2e-3)
+    o3.load_state_dict(sd)
+    for _ in range(2):
+        step(m1, o1)
+        step(m3, o3)
+    for a, b in zip(m1.parameters(), m3.parameters()):
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+
+
+def test_zero1_single_rank_equals_plain_step(q8):
+    n = 7 * 2048 + 100
+    hp = dict(synth.HPARAMS["adamw"])
+    zo = q8.Zero1Optimizer8bit(n, kind="adamw", grad_dtype=torch.bfloat16, device=DEV, **hp)
+    p = synth.params(n).to(DEV)
+    zo.params[:n] = p
+    s1, a1 = synth.zero_state(n, device=DEV)
+    s2, a2 = synth.zero_state(n, device=DEV)
+    for t in range(1, 4):
+        g = synth.grads(n, step=t, dtype="bfloat16").to(DEV)
+        zo.grads[:n] = g
+        zo.step()
+        q8.optim8bit_step("adamw", p, g, s1, s2, a1, a2, step=t, **hp)
+    torch.cuda.synchronize()
+    assert torch.equal(zo.params[:n].view(torch.int32), p.view(torch.int32))
+    assert torch.equal(zo.s1[:n], s1) and torch.equal(zo.absmax2[:a2.numel()], a2)
+
+
+def test_state_bytes_matches_paper_arithmetic(q8):
+    # 8 GB of 32-bit Adam state per 1B params -> 2 GB in 8 bits (+ absmax per block)
+    assert abs(q8.state_bytes(10**9, "adam") / 1e9 - 2.0039) < 1e-3
+    assert abs(q8.state_bytes(10**9, "momentum") / 1e9 - 1.00195) < 1e-4
