@@ -182,7 +182,7 @@ int nsub_variant() {
     static const int v = [] {
         const char* env = std::getenv("Q8_NSUB");
         const int n = env ? std::atoi(env) : 3;
-        return (n == 2 || n == 3 || n == 4) ? n : 3;
+        return (n == 2 || n == 3) ? n : 3;
     }();
     return v;
 }
