@@ -87,23 +87,26 @@ static int code_of(const float T[256], float y) {
 // lut[k] = smallest code of any value in [-1, 1] (signed) / [0, 1] (unsigned) in the bucket;
 // keys beyond that range are unreachable for a normalized value and hold 255 (positive) or 0
 // (negative).  Returns false if some bucket spans more than two codes.
-bool build_bucket_lut(const float T[256], bool is_signed, int shift, int entries, uint8_t* lut) {
+// Keys below key_min are clamped up to key_min by the kernel, so bucket key_min also covers
+// every smaller (non-negative) value.  lut[i] belongs to key key_min + i.
+bool build_bucket_lut(const float T[256], bool is_signed, int shift, int key_min, int entries, uint8_t* lut) {
     const uint32_t one = 0x3f800000u, width = 1u << shift;
-    for (int k = 0; k < entries; ++k) {
-        const uint32_t hi_bits = static_cast<uint32_t>(k) << shift;
+    for (int i = 0; i < entries; ++i) {
+        const int k = key_min + i;
+        const uint32_t hi_bits = (k == key_min && key_min > 0) ? 0u : static_cast<uint32_t>(k) << shift;
         const bool neg = is_signed && (hi_bits & 0x80000000u);
         const uint32_t mlo = hi_bits & 0x7fffffffu;
         if (mlo > one) {                       // |y| > 1: unreachable
-            lut[k] = neg ? 0 : 255;
+            lut[i] = neg ? 0 : 255;
             continue;
         }
-        uint32_t mhi = mlo + width - 1u;
+        uint32_t mhi = (static_cast<uint32_t>(k) << shift & 0x7fffffffu) + width - 1u;
         if (mhi > one) mhi = one;
         const float a = bits_to_float(mlo), b = bits_to_float(mhi);
         const float lo = neg ? -b : a, hi = neg ? -a : b;   // the bucket's value range
         const int c_lo = code_of(T, lo), c_hi = code_of(T, hi);
         if (c_hi - c_lo > 1) return false;
-        lut[k] = static_cast<uint8_t>(c_lo);
+        lut[i] = static_cast<uint8_t>(c_lo);
     }
     return true;
 }

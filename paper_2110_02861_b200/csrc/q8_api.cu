@@ -20,7 +20,7 @@ namespace q8 {
 void build_dynamic_codebook(bool is_signed, float out[256]);
 void build_eytzinger_thresholds(const float Q[256], float out[256]);
 void build_sorted_thresholds(const float Q[256], float out[256]);
-bool build_bucket_lut(const float T[256], bool is_signed, int shift, int entries, uint8_t* lut);
+bool build_bucket_lut(const float T[256], bool is_signed, int shift, int key_min, int entries, uint8_t* lut);
 }  // namespace q8
 
 namespace {
@@ -73,8 +73,9 @@ q8_status device_state(DeviceState** out) {
         q8::build_eytzinger_thresholds(host + q8::kTabQu, host + q8::kTabTu);
         q8::build_sorted_thresholds(host + q8::kTabQu, host + q8::kTabSu);
         uint8_t* lut = reinterpret_cast<uint8_t*>(host + q8::kTabLut);
-        if (!q8::build_bucket_lut(host + q8::kTabSs, true, q8::kShiftS, q8::kLutSBytes, lut) ||
-            !q8::build_bucket_lut(host + q8::kTabSu, false, q8::kShiftU, q8::kLutUBytes, lut + q8::kLutSBytes))
+        if (!q8::build_bucket_lut(host + q8::kTabSs, true, q8::kShiftS, 0, q8::kLutSBytes, lut) ||
+            !q8::build_bucket_lut(host + q8::kTabSu, false, q8::kShiftU, q8::kLutUKeyMin, q8::kLutUBytes,
+                                  lut + q8::kLutSBytes))
             return fail(Q8_ERR_CUDA, "internal: bucket table spans more than two codes");
         float* ptr = nullptr;
         e = cudaMalloc(&ptr, sizeof host);
@@ -182,7 +183,7 @@ int nsub_variant() {
     static const int v = [] {
         const char* env = std::getenv("Q8_NSUB");
         const int n = env ? std::atoi(env) : 3;
-        return (n == 2 || n == 3) ? n : 3;
+        return (n == 2 || n == 3 || n == 4) ? n : 3;
     }();
     return v;
 }

@@ -43,11 +43,13 @@ constexpr int kTabLut = 1536;                     // word offset of the byte tab
 // Bucketed search.  The binary search's first seven levels are replaced by
 // one lookup in a table indexed directly by the leading bits of y, the eighth by a compare:
 //   signed:   key = bits(y) >> 17  (sign, exponent, 6 mantissa bits); 0x6000 keys cover [-1, 1]
-//   unsigned: key = bits(y) >> 16  (exponent, 7 mantissa bits);       0x4000 keys cover [0, 1]
+//   unsigned: key = max(bits(y) >> 16, 0x3400) (exponent, 7 mantissa bits); keys 0x3400-0x3fff
+//             cover [0, 1] (every y < 2^-23 shares bucket 0x3400: all below T_0 = 1.6e-7)
 // LUT[key] = c0 = the smallest code of any y in the bucket.  Every bucket spans at most two
 // codes (checked exhaustively when the tables are built), so code = c0 + [y > T_{c0}].
 constexpr int kShiftS = 17, kShiftU = 16;
-constexpr int kLutSBytes = 0x6000, kLutUBytes = 0x4000;
+constexpr int kLutUKeyMin = 0x3400;
+constexpr int kLutSBytes = 0x6000, kLutUBytes = 0x4000 - kLutUKeyMin;
 constexpr int kTabBytes = kTabLut * 4 + kLutSBytes + kLutUBytes;
 constexpr int kTabFloats = kTabBytes / 4;
 constexpr int SEARCH_EYTZINGER = 0, SEARCH_BUCKET = 1;

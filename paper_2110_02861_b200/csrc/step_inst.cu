@@ -30,6 +30,11 @@ cudaError_t launch_kind(const StepParams<MAXT>& P, const LaunchCtx& ctx) {
     switch (ctx.nsub) {
         case 2: return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, 2>, 2, P.total_blocks, ctx, P,
                                   ctx.tabs);
+        case 4:
+            if constexpr (G != G_F32)
+                return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, 4>, 4, P.total_blocks, ctx, P,
+                                  ctx.tabs);
+            [[fallthrough]];
         default: return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, 3>, 3, P.total_blocks, ctx, P,
                                    ctx.tabs);
     }
