@@ -178,14 +178,16 @@ int search_variant() {
     return v;
 }
 
-// Sub-blocks (256-thread groups, one 2048-element block each) per persistent CTA.
-int nsub_variant() {
-    static const int v = [] {
-        const char* env = std::getenv("Q8_NSUB");
-        const int n = env ? std::atoi(env) : 3;
-        return (n == 2 || n == 3 || n == 4) ? n : 3;
+// Sub-blocks (256-thread groups, one 2048-element block each) per persistent CTA: 4 for 16-bit
+// gradients, 3 for fp32 (shared-memory bound); Q8_NSUB=2|3|4 overrides (tuning).
+int nsub_variant(q8_dtype gdt) {
+    static const int env = [] {
+        const char* e = std::getenv("Q8_NSUB");
+        const int n = e ? std::atoi(e) : 0;
+        return (n >= 2 && n <= 4) ? n : 0;
     }();
-    return v;
+    const int mx = gdt == Q8_F32 ? 3 : 4;
+    return env ? std::min(env, mx) : mx;
 }
 
 std::mutex g_smem_mu;
@@ -194,7 +196,7 @@ const void* g_smem_done[256];
 template <int MAXT>
 q8_status dispatch_step(q8_kind kind, q8_dtype gdt, const q8::StepParams<MAXT>& P, const DeviceState* d,
                         cudaStream_t st) {
-    const q8::LaunchCtx ctx{d->tabs, d->sms, st, search_variant(), nsub_variant()};
+    const q8::LaunchCtx ctx{d->tabs, d->sms, st, search_variant(), nsub_variant(gdt)};
     const q8::StepParams<1>* single = nullptr;
     const q8::StepParams<q8::kMultiMaxT>* multi = nullptr;
     if constexpr (MAXT == 1) single = &P; else multi = &P;
