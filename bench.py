@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--zero1-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-zero1", action="store_true", help="run the ZeRO-1 round trip even at one rank")
     return ap.parse_args()
 
 
@@ -85,7 +86,7 @@ def workload_config(name, world):
 class ClockSampler:
     """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
@@ -118,15 +119,16 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 6:
+            if len(parts) < 7:
                 continue
             try:
                 sm.append(float(parts[0]))
                 mx.append(float(parts[1]))
+                pw.append(float(parts[6]))
             except ValueError:
                 continue
             for nm, v in zip(names, parts[2:6]):
@@ -135,7 +137,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "power_w_median": statistics.median(pw), "samples": len(sm)}
 
 
 # ----------------------------------------------------------------------------- CPU oracle
@@ -221,7 +223,7 @@ def main():
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or "RANK" in os.environ:
         dist.init_process_group("nccl", device_id=dev)
     cfg = workload_config(args.workload, world)
     kind, gdt = cfg["kind"], cfg["grad_dtype"]
@@ -327,7 +329,7 @@ def main():
 
     # ---- ZeRO-1 round trip (N > 1): reduce-scatter bf16 grads -> shard step -> all-gather params
     zero1 = None
-    if world > 1 and args.zero1_steps > 0:
+    if (world > 1 or args.force_zero1) and dist.is_initialized() and args.zero1_steps > 0:
         del gpool
         torch.cuda.empty_cache()
         zo = zero.Zero1Optimizer8bit(n_total, kind=kind, grad_dtype=TORCH_DT[gdt], device=dev, **hp)
@@ -379,7 +381,7 @@ def main():
             "library": q8.version(),
         }
         print(json.dumps(out))
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

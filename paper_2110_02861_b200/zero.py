@@ -65,7 +65,7 @@ class Zero1Optimizer8bit:
         B.optim8bit_step(self.kind, p, g, s1, s2, a1, a2, step=step, **self.hp)
 
     def reduce_scatter(self):
-        if self.world == 1:
+        if not dist.is_initialized():
             self.g_shard.copy_(self.grads[self.lo:self.hi])
             return
         try:
@@ -75,7 +75,7 @@ class Zero1Optimizer8bit:
             self.g_shard.div_(self.world)
 
     def all_gather(self):
-        if self.world > 1:
+        if dist.is_initialized():
             dist.all_gather_into_tensor(self.params, self.p_shard.clone() if not self.params.is_cuda else self.p_shard,
                                         group=self.group)
 
