@@ -79,6 +79,12 @@ typedef struct {
  * rounded once to fp32.  Pure host function.  Errors: INVALID if out_host is NULL. */
 q8_status q8_create_dynamic_codebook(int32_t is_signed, float* out_host);
 
+/* Fill out_host[256] with the linear data type: 256 evenly spaced values over [-1, 1]
+ * (is_signed = 1; -1 + 2i/255) or [0, 1] (is_signed = 0; i/255), computed in double and rounded
+ * once.  The paper's ablation baseline "without dynamic quantization use linear quantization"
+ * (T3 caption).  Pure host function.  Errors: INVALID if out_host is NULL. */
+q8_status q8_create_linear_codebook(int32_t is_signed, float* out_host);
+
 /* Block-wise quantization, Eq.4:
  *   N_b = max_i |x_i| over block b;  y_i = x_i / N_b (IEEE fp32 division; y = 0
  *   when N_b = 0, G7);  codes_i = argmin_j |code_dev[j] - y_i|, ties to the lower index (G6).
@@ -105,6 +111,18 @@ q8_status q8_quantize_blockwise_dynamic(int32_t is_signed, const float* x_dev, f
  * aligned.  blocksize must be 2048. */
 q8_status q8_dequantize_blockwise(const float* code_dev, const uint8_t* codes_dev, const float* absmax_dev,
                                   float* out_dev, int64_t n, int32_t blocksize, void* stream);
+
+/* Tensor-wise quantization, Eq.3: one normalization constant N = max_i |x_i| for
+ * the whole tensor (the cross-core reduction that block-wise quantization avoids), then
+ * codes_i = argmin_j |code_dev[j] - x_i / N| (IEEE division, ties to the lower index).
+ *   absmax_dev [1] fp32 (written: N); other buffers as q8_quantize_blockwise.  Two kernels: a
+ *   grid reduction then the search. */
+q8_status q8_quantize_tensorwise(const float* code_dev, const float* x_dev, float* absmax_dev,
+                                 uint8_t* codes_dev, int64_t n, void* stream);
+
+/* Tensor-wise dequantization: out_i = code_dev[codes_i] * absmax_dev[0]. */
+q8_status q8_dequantize_tensorwise(const float* code_dev, const uint8_t* codes_dev, const float* absmax_dev,
+                                   float* out_dev, int64_t n, void* stream);
 
 /* The fused 8-bit optimizer step (S3; Fig.1), in place, for one tensor:
  * for each block b:

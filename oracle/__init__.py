@@ -54,6 +54,7 @@ def lib():
         u8p = ctypes.POINTER(ctypes.c_uint8)
         i64 = ctypes.c_int64
         l.oracle_dynamic_codebook.argtypes = [ctypes.c_int, f32p]
+        l.oracle_linear_codebook.argtypes = [ctypes.c_int, f32p]
         l.oracle_nearest_code.argtypes = [f32p, ctypes.c_float]
         l.oracle_quantize_blockwise.argtypes = [f32p, f32p, i64, i64, f32p, u8p]
         l.oracle_dequantize_blockwise.argtypes = [f32p, u8p, f32p, i64, i64, f32p]
@@ -80,6 +81,13 @@ def dynamic_codebook(signed: bool) -> np.ndarray:
     rc = lib().oracle_dynamic_codebook(1 if signed else 0, _ptr(out, ctypes.c_float))
     if rc != 0:
         raise RuntimeError("oracle codebook is not 256 distinct ascending values")
+    return out
+
+
+def linear_codebook(signed: bool) -> np.ndarray:
+    """256 evenly spaced binary32 values over [-1, 1] (signed) / [0, 1] (T3 ablation baseline)."""
+    out = np.zeros(256, np.float32)
+    lib().oracle_linear_codebook(1 if signed else 0, _ptr(out, ctypes.c_float))
     return out
 
 

@@ -19,6 +19,7 @@
  * Parity status of every exported function (pins live in tests/test_oracle_*.py):
  *   oracle_dynamic_codebook   pinned: exact rational closed form, invariants,
  *                              golden hashes (tests/golden/)
+ *   oracle_linear_codebook     pinned: even spacing, exact endpoints, symmetry
  *   oracle_nearest_code        pinned: brute-force argmin (numpy) incl. exact ties
  *   oracle_quantize_blockwise  pinned: SPEC worked examples, absmax = np.max|x|,
  *                              half-gap bound, block independence
@@ -102,6 +103,19 @@ int oracle_dynamic_codebook(int is_signed, float out[256]) {
     qsort(out, 256, sizeof(float), cmp_float_asc);
     for (int i = 1; i < 256; i++)
         if (!(out[i - 1] < out[i])) return -1;   /* must be 256 distinct values */
+    return 0;
+}
+
+/*
+ * Linear data type (the ablation baseline "without dynamic quantization use linear
+ * quantization", T3 caption P:214): 256 evenly spaced values, -1 + 2i/255 (signed) or i/255
+ * (unsigned), i = 0..255, evaluated in double and rounded once to binary32.
+ */
+int oracle_linear_codebook(int is_signed, float out[256]) {
+    for (int i = 0; i < 256; i++) {
+        double v = is_signed ? -1.0 + 2.0 * (double)i / 255.0 : (double)i / 255.0;
+        out[i] = (float)v;
+    }
     return 0;
 }
 

@@ -6,11 +6,13 @@ into ``libq8.so``); this package is the thin Python binding plus the torch-facin
 optimizer classes and the ZeRO-1 sharding wrapper.  There is no CPU fallback.
 """
 from ._binding import (BLOCKSIZE, MAX_TENSORS_PER_LAUNCH, Q8Error, TensorList, create_dynamic_codebook,
-                       dequantize_blockwise, hparams, nblocks, optim8bit_step, optim8bit_step_multi,
-                       quantize_blockwise, quantize_blockwise_dynamic, version)
+                       create_linear_codebook, dequantize_blockwise, dequantize_tensorwise, hparams, nblocks,
+                       optim8bit_step, optim8bit_step_multi, quantize_blockwise, quantize_blockwise_dynamic,
+                       quantize_tensorwise, version)
 
 __all__ = [
     "BLOCKSIZE", "MAX_TENSORS_PER_LAUNCH", "Q8Error", "TensorList", "create_dynamic_codebook",
+    "create_linear_codebook", "dequantize_tensorwise", "quantize_tensorwise",
     "dequantize_blockwise", "hparams", "nblocks", "optim8bit_step", "optim8bit_step_multi", "quantize_blockwise",
     "quantize_blockwise_dynamic", "version",
 ]

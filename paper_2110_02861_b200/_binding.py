@@ -21,8 +21,9 @@ BLOCKSIZE = 2048
 KINDS = {"adam": Q8_ADAM, "adamw": Q8_ADAMW, "momentum": Q8_MOMENTUM}
 GDTYPES = {torch.float32: Q8_F32, torch.float16: Q8_F16, torch.bfloat16: Q8_BF16}
 
-EXPORTS = ("q8_create_dynamic_codebook", "q8_quantize_blockwise", "q8_quantize_blockwise_dynamic",
-           "q8_dequantize_blockwise",
+EXPORTS = ("q8_create_dynamic_codebook", "q8_create_linear_codebook", "q8_quantize_blockwise",
+           "q8_quantize_blockwise_dynamic", "q8_dequantize_blockwise", "q8_quantize_tensorwise",
+           "q8_dequantize_tensorwise",
            "q8_optim8bit_step", "q8_optim8bit_step_multi", "q8_last_error", "q8_version")
 
 
@@ -48,6 +49,9 @@ def _load():
     lib = ctypes.CDLL(LIB_PATH)
     vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
     lib.q8_create_dynamic_codebook.argtypes = [i32, vp]
+    lib.q8_create_linear_codebook.argtypes = [i32, vp]
+    lib.q8_quantize_tensorwise.argtypes = [vp, vp, vp, vp, i64, vp]
+    lib.q8_dequantize_tensorwise.argtypes = [vp, vp, vp, vp, i64, vp]
     lib.q8_quantize_blockwise.argtypes = [vp, vp, vp, vp, i64, i32, vp]
     lib.q8_quantize_blockwise_dynamic.argtypes = [i32, vp, vp, vp, i64, i32, vp]
     lib.q8_dequantize_blockwise.argtypes = [vp, vp, vp, vp, i64, i32, vp]
@@ -97,6 +101,42 @@ def create_dynamic_codebook(signed: bool) -> torch.Tensor:
     """Host call: the 256 ascending fp32 values of the (un)signed dynamic data type."""
     out = torch.empty(256, dtype=torch.float32)
     _check(lib.q8_create_dynamic_codebook(1 if signed else 0, out.data_ptr()))
+    return out
+
+
+def create_linear_codebook(signed: bool) -> torch.Tensor:
+    """Host call: the 256 evenly spaced fp32 values of the linear data type (ablation baseline)."""
+    out = torch.empty(256, dtype=torch.float32)
+    _check(lib.q8_create_linear_codebook(1 if signed else 0, out.data_ptr()))
+    return out
+
+
+def quantize_tensorwise(code: torch.Tensor, x: torch.Tensor, absmax: torch.Tensor | None = None,
+                        codes: torch.Tensor | None = None):
+    """Eq.3: one absmax for the whole tensor, then the nearest code of x/N."""
+    n = x.numel()
+    if absmax is None:
+        absmax = torch.empty(1, dtype=torch.float32, device=x.device)
+    if codes is None:
+        codes = torch.empty(n, dtype=torch.uint8, device=x.device)
+    if codes.numel() != n or absmax.numel() < 1 or code.numel() != 256:
+        raise ValueError("size mismatch")
+    _check(lib.q8_quantize_tensorwise(_dev_ptr(code, torch.float32, "code"), _dev_ptr(x, torch.float32, "x"),
+                                      _dev_ptr(absmax, torch.float32, "absmax"), _dev_ptr(codes, torch.uint8, "codes"),
+                                      n, _stream(x.device)))
+    return absmax, codes
+
+
+def dequantize_tensorwise(code: torch.Tensor, codes: torch.Tensor, absmax: torch.Tensor,
+                          out: torch.Tensor | None = None):
+    n = codes.numel()
+    if out is None:
+        out = torch.empty(n, dtype=torch.float32, device=codes.device)
+    if out.numel() != n or absmax.numel() < 1 or code.numel() != 256:
+        raise ValueError("size mismatch")
+    _check(lib.q8_dequantize_tensorwise(_dev_ptr(code, torch.float32, "code"), _dev_ptr(codes, torch.uint8, "codes"),
+                                        _dev_ptr(absmax, torch.float32, "absmax"), _dev_ptr(out, torch.float32, "out"),
+                                        n, _stream(codes.device)))
     return out
 
 

@@ -236,6 +236,60 @@ const char* q8_last_error(void) { return g_last_error.c_str(); }
 
 const char* q8_version(void) { return "q8 0.1 sm_100a"; }
 
+q8_status q8_create_linear_codebook(int32_t is_signed, float* out_host) {
+    if (!out_host) return fail(Q8_ERR_INVALID, "out_host is NULL");
+    for (int i = 0; i < 256; ++i) {
+        // 256 evenly spaced values over [-1, 1] (signed) or [0, 1] (unsigned), each computed in
+        // double and rounded once (linear quantization, T3 caption P:214)
+        const double v = is_signed ? -1.0 + 2.0 * static_cast<double>(i) / 255.0 : static_cast<double>(i) / 255.0;
+        out_host[i] = static_cast<float>(v);
+    }
+    return ok();
+}
+
+q8_status q8_quantize_tensorwise(const float* code_dev, const float* x_dev, float* absmax_dev, uint8_t* codes_dev,
+                                 int64_t n, void* stream) {
+    if (n < 0) return fail(Q8_ERR_INVALID, "n < 0");
+    if (n == 0) return ok();
+    if (!code_dev || !x_dev || !absmax_dev || !codes_dev) return fail(Q8_ERR_INVALID, "NULL buffer with n > 0");
+    if (!aligned(x_dev, 16) || !aligned(codes_dev, 4) || !aligned(absmax_dev, 4) || !aligned(code_dev, 4))
+        return fail(Q8_ERR_INVALID, "misaligned buffer (x 16 B, codes 4 B)");
+    DeviceState* d = nullptr;
+    if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(absmax_dev, 0, sizeof(float), st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(absmax)");
+    const int64_t n4 = (n / 4 + q8::kThreads - 1) / q8::kThreads;
+    const unsigned grid_r = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(n4, 4 * d->sms)));
+    q8::tensor_absmax_kernel<<<grid_r, q8::kThreads, 0, st>>>(x_dev, n, reinterpret_cast<unsigned int*>(absmax_dev));
+    const int64_t nb = (n + q8::kBlock - 1) / q8::kBlock;
+    static int occ = ctas_per_sm(reinterpret_cast<const void*>(q8::quantize_blockwise_kernel<true>));
+    q8::quantize_blockwise_kernel<true><<<static_cast<unsigned>(grid_for(d, occ, nb)), q8::kThreads, 0, st>>>(
+        code_dev, x_dev, absmax_dev, codes_dev, n, nb);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "quantize_tensorwise launch");
+    return ok();
+}
+
+q8_status q8_dequantize_tensorwise(const float* code_dev, const uint8_t* codes_dev, const float* absmax_dev,
+                                   float* out_dev, int64_t n, void* stream) {
+    if (n < 0) return fail(Q8_ERR_INVALID, "n < 0");
+    if (n == 0) return ok();
+    if (!code_dev || !codes_dev || !absmax_dev || !out_dev) return fail(Q8_ERR_INVALID, "NULL buffer with n > 0");
+    if (!aligned(out_dev, 16) || !aligned(codes_dev, 4) || !aligned(absmax_dev, 4) || !aligned(code_dev, 4))
+        return fail(Q8_ERR_INVALID, "misaligned buffer (out 16 B, codes 4 B)");
+    DeviceState* d = nullptr;
+    if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    const int64_t nb = (n + q8::kBlock - 1) / q8::kBlock;
+    static int occ = ctas_per_sm(reinterpret_cast<const void*>(q8::dequantize_blockwise_kernel<true>));
+    q8::dequantize_blockwise_kernel<true><<<static_cast<unsigned>(grid_for(d, occ, nb)), q8::kThreads, 0,
+                                            static_cast<cudaStream_t>(stream)>>>(code_dev, codes_dev, absmax_dev,
+                                                                                 out_dev, n, nb);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "dequantize_tensorwise launch");
+    return ok();
+}
+
 q8_status q8_create_dynamic_codebook(int32_t is_signed, float* out_host) {
     if (!out_host) return fail(Q8_ERR_INVALID, "out_host is NULL");
     q8::build_dynamic_codebook(is_signed != 0, out_host);
@@ -253,8 +307,8 @@ q8_status q8_quantize_blockwise(const float* code_dev, const float* x_dev, float
     DeviceState* d = nullptr;
     if (q8_status s = device_state(&d); s != Q8_OK) return s;
     const int64_t nb = (n + q8::kBlock - 1) / q8::kBlock;
-    static int occ = ctas_per_sm(reinterpret_cast<const void*>(q8::quantize_blockwise_kernel));
-    q8::quantize_blockwise_kernel<<<static_cast<unsigned>(grid_for(d, occ, nb)), q8::kThreads, 0,
+    static int occ = ctas_per_sm(reinterpret_cast<const void*>(q8::quantize_blockwise_kernel<false>));
+    q8::quantize_blockwise_kernel<false><<<static_cast<unsigned>(grid_for(d, occ, nb)), q8::kThreads, 0,
                                     static_cast<cudaStream_t>(stream)>>>(code_dev, x_dev, absmax_dev, codes_dev, n, nb);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "quantize_blockwise_kernel launch");
@@ -301,8 +355,8 @@ q8_status q8_dequantize_blockwise(const float* code_dev, const uint8_t* codes_de
     DeviceState* d = nullptr;
     if (q8_status s = device_state(&d); s != Q8_OK) return s;
     const int64_t nb = (n + q8::kBlock - 1) / q8::kBlock;
-    static int occ = ctas_per_sm(reinterpret_cast<const void*>(q8::dequantize_blockwise_kernel));
-    q8::dequantize_blockwise_kernel<<<static_cast<unsigned>(grid_for(d, occ, nb)), q8::kThreads, 0,
+    static int occ = ctas_per_sm(reinterpret_cast<const void*>(q8::dequantize_blockwise_kernel<false>));
+    q8::dequantize_blockwise_kernel<false><<<static_cast<unsigned>(grid_for(d, occ, nb)), q8::kThreads, 0,
                                       static_cast<cudaStream_t>(stream)>>>(code_dev, codes_dev, absmax_dev, out_dev, n,
                                                                             nb);
     cudaError_t e = cudaGetLastError();

@@ -32,6 +32,9 @@ __device__ __forceinline__ void stage_generic_table(const float* __restrict__ co
 }
 
 // Block-wise quantization, Eq.4 -- a8.  IEEE division for y = x / N_b.
+// TW (tensor-wise, Eq.3): N = absmax[0], the maximum over the whole tensor computed by
+// tensor_absmax_kernel beforehand; no per-block reduction, absmax is not written.
+template <bool TW>
 __global__ void __launch_bounds__(kThreads) quantize_blockwise_kernel(const float* __restrict__ code,
                                                                       const float* __restrict__ x,
                                                                       float* __restrict__ absmax,
@@ -60,7 +63,7 @@ __global__ void __launch_bounds__(kThreads) quantize_blockwise_kernel(const floa
 #pragma unroll
             for (int e = 0; e < kVec; ++e) mx = fmaxf(mx, fabsf(v[c][e]));
         }
-        const float N = block_max(mx, red[parity]);
+        const float N = TW ? absmax[0] : block_max(mx, red[parity]);
 #pragma unroll
         for (int c = 0; c < kGroups; ++c) {
             const int64_t i0 = base + c * (kThreads * kVec) + tid * kVec;
@@ -78,11 +81,36 @@ __global__ void __launch_bounds__(kThreads) quantize_blockwise_kernel(const floa
                     if (i0 + e < n) codes[i0 + e] = static_cast<uint8_t>(o >> (8 * e));
             }
         }
-        if (tid == 0) absmax[b] = N;
+        if (!TW && tid == 0) absmax[b] = N;
     }
 }
 
-// Block-wise dequantization: out = Q[code] * N_b -- a8.
+// Tensor-wise absmax N = max |T| (Eq.3; the "reduction over the entire tensor" that
+// block-wise quantization avoids): per-CTA REDUX/shared reduction, then one atomicMax
+// per CTA on the float bits (non-negative floats order like unsigned integers).  *out must be
+// 0 on entry.
+__global__ void __launch_bounds__(kThreads) tensor_absmax_kernel(const float* __restrict__ x, int64_t n,
+                                                                 unsigned int* __restrict__ out) {
+    __shared__ unsigned int red[kWarps];
+    float mx = 0.0f;
+    const int64_t n4 = n / 4;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n4;
+         i += static_cast<int64_t>(gridDim.x) * kThreads) {
+        const float4 v = ld_stream_f4(x + 4 * i);
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+    if (blockIdx.x == 0 && threadIdx.x < n - 4 * n4) mx = fmaxf(mx, fabsf(x[4 * n4 + threadIdx.x]));
+    const unsigned int w = __reduce_max_sync(0xffffffffu, __float_as_uint(mx));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const unsigned int v = __reduce_max_sync(0xffffffffu, threadIdx.x < kWarps ? red[threadIdx.x] : 0u);
+        if (threadIdx.x == 0) atomicMax(out, v);
+    }
+}
+
+// Block-wise dequantization: out = Q[code] * N_b -- a8.  TW: N = absmax[0] for all.
+template <bool TW>
 __global__ void __launch_bounds__(kThreads) dequantize_blockwise_kernel(const float* __restrict__ code,
                                                                         const uint8_t* __restrict__ codes,
                                                                         const float* __restrict__ absmax,
@@ -95,7 +123,7 @@ __global__ void __launch_bounds__(kThreads) dequantize_blockwise_kernel(const fl
     for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x) {
         const int64_t base = b * kBlock;
         const bool full = base + kBlock <= n;
-        const float N = absmax[b];
+        const float N = absmax[TW ? 0 : b];
 #pragma unroll
         for (int c = 0; c < kGroups; ++c) {
             const int64_t i0 = base + c * (kThreads * kVec) + tid * kVec;

@@ -98,3 +98,10 @@ def test_multi_validation():
     assert rc == B.Q8_ERR_INVALID and "tensor 1" in B.lib.q8_last_error().decode()
     assert B.lib.q8_optim8bit_step_multi(B.Q8_ADAM, B.Q8_F16, arr, -1, 2048, ctypes.byref(_hp()), 1,
                                          None) == B.Q8_ERR_INVALID
+
+
+@pytest.mark.parametrize("signed", [True, False])
+def test_host_linear_codebook_matches_oracle(signed):
+    a = q8.create_linear_codebook(signed).numpy()
+    b = oracle.linear_codebook(signed)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))

@@ -296,3 +296,22 @@ def test_errors_surface_as_exceptions(q8):
         q8.optim8bit_step("adam", p[1:], g[1:], s[1:], s[1:], a, a, lr=1e-3, step=1)  # misaligned p
     with pytest.raises(q8.Q8Error):
         q8.optim8bit_step("adam", p, g, s, s, a, a, lr=1e-3, step=1, blocksize=4096)
+
+
+@pytest.mark.parametrize("n", [1, 17, 2049, 3 * 2048 + 5, 1_000_000])
+@pytest.mark.parametrize("table", ["dynamic_signed", "linear_signed", "linear_unsigned"])
+def test_tensorwise_codec_bit_exact(q8, n, table):
+    """Eq.3: one absmax for the whole tensor (oracle: block size = n)."""
+    Q = {"dynamic_signed": oracle.dynamic_codebook(True), "linear_signed": oracle.linear_codebook(True),
+         "linear_unsigned": oracle.linear_codebook(False)}[table]
+    x = synth.params(n, seed=n + 3, std=1.0)
+    if table == "linear_unsigned":
+        x = x.abs()
+    if n > 10:
+        x[n // 2] = 37.0  # an outlier dominates the single normalization constant (P:112)
+    code_dev = torch.from_numpy(Q).to(DEV)
+    a_g, c_g = q8.quantize_tensorwise(code_dev, x.to(DEV))
+    a_r, c_r = oracle.quantize_blockwise(Q, x.numpy(), blocksize=n)
+    assert_same(a_g, a_r, "absmax")
+    assert_same(c_g, c_r, "codes")
+    assert_same(q8.dequantize_tensorwise(code_dev, c_g, a_g), oracle.dequantize_blockwise(Q, c_r, a_r, n), "deq")

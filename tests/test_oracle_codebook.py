@@ -104,3 +104,17 @@ def test_every_code_round_trips(signed):
     """quantize(dequantize(i)) = i for every code (BASELINE north_star invariant)."""
     Q = oracle.dynamic_codebook(signed)
     assert np.array_equal(oracle.nearest_code(Q, Q), np.arange(256, dtype=np.uint8))
+
+
+@pytest.mark.parametrize("signed", [True, False])
+def test_linear_codebook(signed):
+    """Linear type (T3 caption): 256 evenly spaced values with exact endpoints."""
+    Q = oracle.linear_codebook(signed).astype(np.float64)
+    assert Q.size == 256 and np.all(np.diff(Q) > 0)
+    assert Q[-1] == 1.0 and Q[0] == (-1.0 if signed else 0.0)
+    step = (Q[-1] - Q[0]) / 255
+    assert np.max(np.abs(np.diff(Q) - step)) <= 2 * np.spacing(np.float32(1.0))   # even spacing
+    if signed:
+        assert np.array_equal(Q, -Q[::-1])                                           # symmetric
+    assert np.array_equal(oracle.nearest_code(oracle.linear_codebook(signed), oracle.linear_codebook(signed)),
+                          np.arange(256, dtype=np.uint8))
