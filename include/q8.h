@@ -155,6 +155,24 @@ q8_status q8_optim8bit_step_multi(q8_kind kind, q8_dtype g_dtype, const q8_tenso
                                   int32_t num_tensors, int32_t blocksize, const q8_hparams* hp, int64_t step,
                                   void* stream);
 
+/* One tensor of a 32-bit-state step: fp32 states m, r instead of codes + absmax (r unused,
+ * may be NULL, for Q8_MOMENTUM).  All device pointers, 16-byte aligned. */
+typedef struct {
+    float* p;
+    const void* g;
+    float* m;
+    float* r;
+    int64_t n;
+} q8_tensor32;
+
+/* The same fp32 update as q8_optim8bit_step (Eq.1/Eq.2, G8-G12, identical operation order) with
+ * the states kept in 32 bits, over many tensors: the paper keeps the Stable Embedding layer's
+ * optimizer states in 32 bits ("the only layer that uses 32-bit optimizer states", S3.3
+ * P:124-125).  m, r are read-modify-write fp32 [n]; zero is the initial state.  Validation as
+ * q8_optim8bit_step_multi. */
+q8_status q8_optim32bit_step_multi(q8_kind kind, q8_dtype g_dtype, const q8_tensor32* tensors_host,
+                                   int32_t num_tensors, const q8_hparams* hp, int64_t step, void* stream);
+
 /* Thread-local description of the last error ("" after success). */
 const char* q8_last_error(void);
 

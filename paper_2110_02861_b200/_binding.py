@@ -24,7 +24,7 @@ GDTYPES = {torch.float32: Q8_F32, torch.float16: Q8_F16, torch.bfloat16: Q8_BF16
 EXPORTS = ("q8_create_dynamic_codebook", "q8_create_linear_codebook", "q8_quantize_blockwise",
            "q8_quantize_blockwise_dynamic", "q8_dequantize_blockwise", "q8_quantize_tensorwise",
            "q8_dequantize_tensorwise",
-           "q8_optim8bit_step", "q8_optim8bit_step_multi", "q8_last_error", "q8_version")
+           "q8_optim8bit_step", "q8_optim8bit_step_multi", "q8_optim32bit_step_multi", "q8_last_error", "q8_version")
 
 
 class Q8Error(RuntimeError):
@@ -36,6 +36,11 @@ class Q8Error(RuntimeError):
 class HParams(ctypes.Structure):
     _fields_ = [("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
                 ("eps", ctypes.c_double), ("weight_decay", ctypes.c_double), ("bias_correction", ctypes.c_int32)]
+
+
+class TensorDesc32(ctypes.Structure):
+    _fields_ = [("p", ctypes.c_void_p), ("g", ctypes.c_void_p), ("m", ctypes.c_void_p), ("r", ctypes.c_void_p),
+                ("n", ctypes.c_int64)]
 
 
 class TensorDesc(ctypes.Structure):
@@ -58,6 +63,8 @@ def _load():
     lib.q8_optim8bit_step.argtypes = [i32, vp, vp, i32, vp, vp, vp, vp, i64, i32, ctypes.POINTER(HParams), i64, vp]
     lib.q8_optim8bit_step_multi.argtypes = [i32, i32, ctypes.POINTER(TensorDesc), i32, i32,
                                             ctypes.POINTER(HParams), i64, vp]
+    lib.q8_optim32bit_step_multi.argtypes = [i32, i32, ctypes.POINTER(TensorDesc32), i32, ctypes.POINTER(HParams),
+                                             i64, vp]
     for f in EXPORTS[:-2]:
         getattr(lib, f).restype = ctypes.c_int
     lib.q8_last_error.restype = ctypes.c_char_p
@@ -243,3 +250,28 @@ def optim8bit_step_multi(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1e-8,
         hp = hparams(lr, beta1, beta2, eps, weight_decay, bias_correction)
     _check(lib.q8_optim8bit_step_multi(kind, tl.gdtype, tl.arr, tl.count, blocksize, ctypes.byref(hp), int(step),
                                        _stream(tl.device)))
+
+
+def optim32bit_step_multi(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0,
+                          bias_correction=True, step=1, hp: HParams | None = None):
+    """The same fp32 update with 32-bit states (m, r fp32 tensors): entries (p, g, m, r_or_None)."""
+    kind = KINDS.get(kind, kind)
+    entries = list(tensors)
+    if not entries:
+        return
+    arr = (TensorDesc32 * len(entries))()
+    gd = None
+    for i, (p, g, m, r) in enumerate(entries):
+        n = p.numel()
+        if g.numel() != n or m.numel() != n or (r is not None and r.numel() != n):
+            raise ValueError(f"tensor {i}: size mismatch")
+        if gd is None:
+            gd = GDTYPES[g.dtype]
+        elif GDTYPES[g.dtype] != gd:
+            raise ValueError("all gradients of one launch must share a dtype")
+        arr[i] = TensorDesc32(_dev_ptr(p, torch.float32, "p"), _dev_ptr(g, None, "g"), _dev_ptr(m, torch.float32, "m"),
+                              _dev_ptr(r, torch.float32, "r"), n)
+    if hp is None:
+        hp = hparams(lr, beta1, beta2, eps, weight_decay, bias_correction)
+    _check(lib.q8_optim32bit_step_multi(kind, gd, arr, len(entries), ctypes.byref(hp), int(step),
+                                        _stream(entries[0][0].device)))

@@ -15,6 +15,7 @@
 #include "q8_codec.cuh"
 #include "q8_launch.h"
 #include "q8_step_kernel.cuh"
+#include "q8_step32_kernel.cuh"
 
 namespace q8 {
 void build_dynamic_codebook(bool is_signed, float out[256]);
@@ -414,6 +415,79 @@ q8_status q8_optim8bit_step_multi(q8_kind kind, q8_dtype g_dtype, const q8_tenso
         P.block_start[k] = blocks;
         P.total_blocks = blocks;
         if (q8_status s = dispatch_step<MAXT>(kind, g_dtype, P, d, static_cast<cudaStream_t>(stream)); s != Q8_OK)
+            return s;
+    }
+    return ok();
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- 32-bit-state step
+
+namespace {
+
+q8_status validate_tensor32(q8_kind kind, const q8_tensor32& t, int idx) {
+    if (t.n < 0) return fail(Q8_ERR_INVALID, "tensor %d: n < 0", idx);
+    if (t.n == 0) return Q8_OK;
+    if (!t.p || !t.g || !t.m || (kind != Q8_MOMENTUM && !t.r))
+        return fail(Q8_ERR_INVALID, "tensor %d: NULL buffer with n > 0", idx);
+    if (!aligned(t.p, 16) || !aligned(t.g, 16) || !aligned(t.m, 16) || (kind != Q8_MOMENTUM && !aligned(t.r, 16)))
+        return fail(Q8_ERR_INVALID, "tensor %d: buffers must be 16-byte aligned", idx);
+    return Q8_OK;
+}
+
+template <int MAXT>
+q8_status launch_step32(q8_kind kind, q8_dtype gdt, const q8::StepParams<MAXT>& P, const DeviceState* d,
+                        cudaStream_t st) {
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(P.total_blocks, 8LL * d->sms));
+#define Q8_CASE32(K, G)                                                                     \
+    if (kind == K && gdt == G) {                                                            \
+        q8::optim32bit_step_kernel<K, G, MAXT><<<grid, q8::kThreads, 0, st>>>(P);             \
+        cudaError_t e = cudaGetLastError();                                                 \
+        return e == cudaSuccess ? Q8_OK : cuda_fail(e, "optim32bit_step_kernel launch");     \
+    }
+    Q8_CASE32(Q8_ADAM, Q8_F32) Q8_CASE32(Q8_ADAM, Q8_F16) Q8_CASE32(Q8_ADAM, Q8_BF16)
+    Q8_CASE32(Q8_ADAMW, Q8_F32) Q8_CASE32(Q8_ADAMW, Q8_F16) Q8_CASE32(Q8_ADAMW, Q8_BF16)
+    Q8_CASE32(Q8_MOMENTUM, Q8_F32) Q8_CASE32(Q8_MOMENTUM, Q8_F16) Q8_CASE32(Q8_MOMENTUM, Q8_BF16)
+#undef Q8_CASE32
+    return fail(Q8_ERR_INVALID, "bad kind/dtype");
+}
+
+}  // namespace
+
+extern "C" {
+
+q8_status q8_optim32bit_step_multi(q8_kind kind, q8_dtype g_dtype, const q8_tensor32* tensors_host,
+                                   int32_t num_tensors, const q8_hparams* hp, int64_t step, void* stream) {
+    if (q8_status s = check_common(g_dtype, q8::kBlock); s != Q8_OK) return s;
+    if (q8_status s = validate_hparams(kind, hp, step); s != Q8_OK) return s;
+    if (num_tensors < 0) return fail(Q8_ERR_INVALID, "num_tensors < 0");
+    if (num_tensors > 0 && !tensors_host) return fail(Q8_ERR_INVALID, "tensors_host is NULL");
+    for (int i = 0; i < num_tensors; ++i)
+        if (q8_status s = validate_tensor32(kind, tensors_host[i], i); s != Q8_OK) return s;
+    DeviceState* d = nullptr;
+    if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    constexpr int MAXT = Q8_MAX_TENSORS_PER_LAUNCH;
+    static thread_local q8::StepParams<MAXT> P;
+    P.s = make_scalars(hp, step);
+    int i = 0;
+    while (i < num_tensors) {
+        int k = 0;
+        int64_t blocks = 0;
+        for (; i < num_tensors && k < MAXT; ++i) {
+            const q8_tensor32& t = tensors_host[i];
+            if (t.n == 0) continue;
+            P.t[k] = q8::TensorDesc{t.p, t.g, reinterpret_cast<uint8_t*>(t.m), reinterpret_cast<uint8_t*>(t.r),
+                                    nullptr, nullptr, t.n};
+            P.block_start[k] = blocks;
+            blocks += (t.n + q8::kBlock - 1) / q8::kBlock;
+            ++k;
+        }
+        if (k == 0) break;
+        P.num_tensors = k;
+        P.block_start[k] = blocks;
+        P.total_blocks = blocks;
+        if (q8_status s = launch_step32<MAXT>(kind, g_dtype, P, d, static_cast<cudaStream_t>(stream)); s != Q8_OK)
             return s;
     }
     return ok();

@@ -3,7 +3,9 @@ change", P:7 / P:28: swap the optimizer class).
 
 Each parameter keeps its optimizer state as 8-bit codes plus one fp32 absmax per 2048-element
 block (S3.1): ``s1``/``absmax1`` for the first state (signed dynamic tree type),
-``s2``/``absmax2`` for Adam's second state (unsigned dynamic type).  A step groups all
+``s2``/``absmax2`` for Adam's second state (unsigned dynamic type).  Tensors marked with
+``_q8_optim_bits = 32`` (the StableEmbedding weight, S3.3 P:124) or in a param group with
+``optim_bits=32`` keep fp32 states ``m``/``r`` instead (``q8_optim32bit_step_multi``).  A step groups all
 parameters that have gradients by gradient dtype and calls ``q8_optim8bit_step_multi`` once
 per group (one kernel launch per <= 384 tensors).  Parameters must be fp32, contiguous and
 16-byte aligned on a CUDA device; there is no CPU path.
@@ -25,25 +27,38 @@ class _Optimizer8bit(torch.optim.Optimizer):
                                       bias_correction=bias_correction))
         self._lists = {}
 
-    def _state_for(self, p: torch.Tensor):
+    @staticmethod
+    def _bits(p: torch.Tensor, group) -> int:
+        # per-tensor override (StableEmbedding sets _q8_optim_bits = 32, S3.3 P:124) or group key
+        return int(getattr(p, "_q8_optim_bits", None) or group.get("optim_bits", 8))
+
+    def _state_for(self, p: torch.Tensor, bits: int):
         st = self.state[p]
         if not st:
             if p.dtype != torch.float32 or not p.is_cuda:
                 raise TypeError("8-bit optimizers update fp32 CUDA parameters")
             n = p.numel()
-            nb = B.nblocks(n)
             st["step"] = 0
-            st["s1"] = torch.zeros(n, dtype=torch.uint8, device=p.device)
-            st["absmax1"] = torch.zeros(nb, dtype=torch.float32, device=p.device)
-            if self.kind != "momentum":
-                st["s2"] = torch.zeros(n, dtype=torch.uint8, device=p.device)
-                st["absmax2"] = torch.zeros(nb, dtype=torch.float32, device=p.device)
+            if bits == 32:
+                st["m"] = torch.zeros(n, dtype=torch.float32, device=p.device)
+                if self.kind != "momentum":
+                    st["r"] = torch.zeros(n, dtype=torch.float32, device=p.device)
+            else:
+                nb = B.nblocks(n)
+                st["s1"] = torch.zeros(n, dtype=torch.uint8, device=p.device)
+                st["absmax1"] = torch.zeros(nb, dtype=torch.float32, device=p.device)
+                if self.kind != "momentum":
+                    st["s2"] = torch.zeros(n, dtype=torch.uint8, device=p.device)
+                    st["absmax2"] = torch.zeros(nb, dtype=torch.float32, device=p.device)
         return st
 
     def load_state_dict(self, state_dict):
         # torch casts floating-point-param state to the param dtype; codes must stay uint8
         super().load_state_dict(state_dict)
         for st in self.state.values():
+            for k in ("m", "r"):
+                if k in st:
+                    st[k] = st[k].to(torch.float32).contiguous()
             for k in ("s1", "s2"):
                 if k in st:
                     st[k] = st[k].to(torch.uint8).contiguous()
@@ -61,17 +76,21 @@ class _Optimizer8bit(torch.optim.Optimizer):
             with torch.enable_grad():
                 loss = closure()
         for group in self.param_groups:
-            buckets = {}
+            buckets, buckets32 = {}, {}
             for p in group["params"]:
                 if p.grad is None:
                     continue
                 if p.grad.is_sparse:
                     raise TypeError("sparse gradients are not supported")
-                st = self._state_for(p)
+                bits = self._bits(p, group)
+                st = self._state_for(p, bits)
                 st["step"] += 1
                 g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
-                buckets.setdefault((g.dtype, st["step"]), []).append(
-                    (p, g, st["s1"], st.get("s2"), st["absmax1"], st.get("absmax2")))
+                if bits == 32:
+                    buckets32.setdefault((g.dtype, st["step"]), []).append((p, g, st["m"], st.get("r")))
+                else:
+                    buckets.setdefault((g.dtype, st["step"]), []).append(
+                        (p, g, st["s1"], st.get("s2"), st["absmax1"], st.get("absmax2")))
             b1, b2 = group["betas"]
             hp = B.hparams(group["lr"], b1, b2, group["eps"], group["weight_decay"], group["bias_correction"])
             for (_, step), entries in buckets.items():
@@ -83,6 +102,8 @@ class _Optimizer8bit(torch.optim.Optimizer):
                         self._lists.clear()
                     self._lists[key] = tl
                 B.optim8bit_step_multi(self.kind, tl, lr=group["lr"], step=step, hp=hp)
+            for (_, step), entries in buckets32.items():
+                B.optim32bit_step_multi(self.kind, entries, lr=group["lr"], step=step, hp=hp)
         return loss
 
 

@@ -101,3 +101,58 @@ def test_state_bytes_matches_paper_arithmetic(q8):
     # 8 GB of 32-bit Adam state per 1B params -> 2 GB in 8 bits (+ absmax per block)
     assert abs(q8.state_bytes(10**9, "adam") / 1e9 - 2.0039) < 1e-3
     assert abs(q8.state_bytes(10**9, "momentum") / 1e9 - 1.00195) < 1e-4
+
+
+@pytest.mark.parametrize("kind", ["adam", "adamw", "momentum"])
+@pytest.mark.parametrize("gdt", ["float32", "bfloat16"])
+def test_32bit_state_step_matches_oracle(q8, kind, gdt):
+    """q8_optim32bit_step_multi == the oracle's 32-bit step (pinned to torch.optim), bit for bit."""
+    hp = dict(synth.HPARAMS[kind])
+    sizes = [1, 2048 * 3 + 7, 100_000]
+    ents, refs = [], []
+    for i, n in enumerate(sizes):
+        p = synth.params(n, seed=i)
+        m = synth.params(n, seed=50 + i, std=1e-3)
+        r = synth.params(n, seed=90 + i, std=1e-3).abs() ** 2
+        ents.append([p.to(DEV), None, m.to(DEV), r.to(DEV) if kind != "momentum" else None])
+        refs.append([p.numpy().copy(), m.numpy().copy(), r.numpy().copy()])
+    for t in (1, 2):
+        gs = [synth.grads(n, step=t, seed=i, dtype=gdt) for i, n in enumerate(sizes)]
+        q8.optim32bit_step_multi(kind, [(e[0], g.to(DEV), e[2], e[3]) for e, g in zip(ents, gs)], step=t, **hp)
+        for ref, g in zip(refs, gs):
+            oracle.optim32bit_step(kind, ref[0], synth.to_f32_numpy(g), ref[1],
+                                   ref[2] if kind != "momentum" else None, step=t, **hp)
+    torch.cuda.synchronize()
+    for e, ref in zip(ents, refs):
+        assert np.array_equal(e[0].cpu().numpy().view(np.uint32), ref[0].view(np.uint32))
+        assert np.array_equal(e[2].cpu().numpy().view(np.uint32), ref[1].view(np.uint32))
+        if kind != "momentum":
+            assert np.array_equal(e[3].cpu().numpy().view(np.uint32), ref[2].view(np.uint32))
+
+
+def test_stable_embedding_keeps_32bit_states(q8):
+    """the embedding layer's states stay 32-bit, the rest 8-bit; both match the oracle."""
+    torch.manual_seed(1)
+    emb = q8.StableEmbedding(500, 64).to(DEV)
+    lin = torch.nn.Linear(64, 40).to(DEV)
+    params = list(emb.parameters()) + list(lin.parameters())
+    ref = [p.detach().cpu().numpy().copy().reshape(-1) for p in params]
+    opt = q8.Adam8bit(params, lr=1e-3)
+    st32 = {0: (np.zeros(ref[0].size, np.float32), np.zeros(ref[0].size, np.float32))}
+    st8 = {i: [np.zeros(r.size, np.uint8), np.zeros(r.size, np.uint8), np.zeros((r.size + 2047) // 2048, np.float32),
+               np.zeros((r.size + 2047) // 2048, np.float32)] for i, r in enumerate(ref) if i > 0}
+    hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, bias_correction=True)
+    x = torch.randint(0, 500, (16, 12), device=DEV)
+    for t in (1, 2, 3):
+        opt.zero_grad()
+        lin(emb(x)).square().mean().backward()
+        grads = [p.grad.detach().cpu().numpy().copy().reshape(-1) for p in params]
+        opt.step()
+        oracle.optim32bit_step("adam", ref[0], grads[0], st32[0][0], st32[0][1], step=t, **hp)
+        for i in st8:
+            s1, s2, a1, a2 = st8[i]
+            oracle.optim8bit_step("adam", ref[i], grads[i], s1, s2, a1, a2, step=t, **hp)
+    assert "m" in opt.state[emb.weight] and "s1" not in opt.state[emb.weight]
+    assert "s1" in opt.state[lin.weight]
+    for p, r in zip(params, ref):
+        assert np.array_equal(p.detach().cpu().numpy().reshape(-1).view(np.uint32), r.view(np.uint32))
