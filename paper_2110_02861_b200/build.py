@@ -23,7 +23,7 @@ NVCC_FLAGS = ARCH + [
     # IEEE fp32 everywhere: bit-exact parity with the oracle depends on it (G9)
     "-prec-div=true", "-prec-sqrt=true", "-ftz=false", "-fmad=false",
     "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v,-warn-spills",
-]
+] + os.environ.get("Q8_EXTRA_NVCC_FLAGS", "").split()
 
 
 def _obj(src, defs):
@@ -57,7 +57,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
                 raise RuntimeError(f"nvcc failed on {src} {defs}")
-    tmp = LIB + f".tmp{os.getpid()}"
+    lib = os.environ.get("Q8_LIB_OUT", LIB)
+    tmp = lib + f".tmp{os.getpid()}"
     link = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp] + [_obj(s, d) for s, d in UNITS]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
@@ -65,8 +66,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc link failed for libq8.so")
     if verbose:
         sys.stderr.write("".join(logs))
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -197,7 +197,12 @@ const void* g_smem_done[256];
 template <int MAXT>
 q8_status dispatch_step(q8_kind kind, q8_dtype gdt, const q8::StepParams<MAXT>& P, const DeviceState* d,
                         cudaStream_t st) {
-    const q8::LaunchCtx ctx{d->tabs, d->sms, st, search_variant(), nsub_variant(gdt)};
+    static const int subt = [] {
+        const char* e = std::getenv("Q8_SUBT");
+        const int v = e ? std::atoi(e) : 0;
+        return (v == 128 || v == 256) ? v : 0;
+    }();
+    const q8::LaunchCtx ctx{d->tabs, d->sms, st, search_variant(), nsub_variant(gdt), subt};
     const q8::StepParams<1>* single = nullptr;
     const q8::StepParams<q8::kMultiMaxT>* multi = nullptr;
     if constexpr (MAXT == 1) single = &P; else multi = &P;
@@ -335,10 +340,10 @@ q8_status q8_quantize_blockwise_dynamic(int32_t is_signed, const float* x_dev, f
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((nb + 2) / 3, d->sms));
     if (is_signed)
-        q8::quantize_blockwise_dynamic_kernel<true, 3><<<grid, 3 * q8::kSubThreads, smem, st>>>(d->tabs, x_dev,
+        q8::quantize_blockwise_dynamic_kernel<true, 3><<<grid, 3 * q8::kQDynSubThreads, smem, st>>>(d->tabs, x_dev,
                                                                                              absmax_dev, codes_dev, n, nb);
     else
-        q8::quantize_blockwise_dynamic_kernel<false, 3><<<grid, 3 * q8::kSubThreads, smem, st>>>(d->tabs, x_dev,
+        q8::quantize_blockwise_dynamic_kernel<false, 3><<<grid, 3 * q8::kQDynSubThreads, smem, st>>>(d->tabs, x_dev,
                                                                                               absmax_dev, codes_dev, n, nb);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "quantize_blockwise_dynamic_kernel launch");

@@ -14,6 +14,7 @@ struct LaunchCtx {
     cudaStream_t stream;
     int search;  // SEARCH_BUCKET or SEARCH_EYTZINGER
     int nsub;    // 2, 3 or 4 sub-blocks per CTA
+    int subt;    // threads per sub-block (128 or 256); 0 = default for the gradient dtype
 };
 
 constexpr int kMultiMaxT = 384;

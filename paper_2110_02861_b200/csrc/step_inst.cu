@@ -11,33 +11,42 @@ namespace q8 {
 namespace {
 
 template <typename Kern, typename... Args>
-cudaError_t persistent(Kern fn, int nsub, int64_t work_blocks, const LaunchCtx& ctx, const Args&... args) {
+cudaError_t persistent(Kern fn, int nsub, int subt, int64_t work_blocks, const LaunchCtx& ctx, const Args&... args) {
     const int smem = step_smem_bytes(nsub, Q8_GDT);
     cudaError_t e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
     if (e != cudaSuccess) return e;
     int64_t grid = (work_blocks + nsub - 1) / nsub;
     if (grid > ctx.sms) grid = ctx.sms;
-    fn<<<static_cast<unsigned>(grid), nsub * kSubThreads, smem, ctx.stream>>>(args...);
+    fn<<<static_cast<unsigned>(grid), nsub * subt, smem, ctx.stream>>>(args...);
     return cudaGetLastError();
+}
+
+// Sub-block size: 128 threads x 16 elements for 16-bit gradients (4 sub-blocks, 16 warps per
+// SM: the per-block overhead is amortized over more elements), 256 x 8 for fp32 gradients (their
+// 20 KB stages allow only 3 sub-blocks, so more warps per sub-block).  Q8_SUBT overrides.
+template <int KIND, int MAXT, int SUBT>
+cudaError_t launch_kind_t(const StepParams<MAXT>& P, const LaunchCtx& ctx) {
+    constexpr int G = Q8_GDT;
+    if (ctx.search == SEARCH_EYTZINGER)  // reference variant: one configuration
+        return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_EYTZINGER, 3, SUBT>, 3, SUBT, P.total_blocks,
+                          ctx, P, ctx.tabs);
+    switch (ctx.nsub) {
+        case 2: return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, 2, SUBT>, 2, SUBT,
+                                  P.total_blocks, ctx, P, ctx.tabs);
+        case 4:
+            if constexpr (G != G_F32)
+                return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, 4, SUBT>, 4, SUBT,
+                                  P.total_blocks, ctx, P, ctx.tabs);
+            [[fallthrough]];
+        default: return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, 3, SUBT>, 3, SUBT,
+                                   P.total_blocks, ctx, P, ctx.tabs);
+    }
 }
 
 template <int KIND, int MAXT>
 cudaError_t launch_kind(const StepParams<MAXT>& P, const LaunchCtx& ctx) {
-    constexpr int G = Q8_GDT;
-    if (ctx.search == SEARCH_EYTZINGER)  // reference variant: one configuration
-        return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_EYTZINGER, 3>, 3, P.total_blocks, ctx, P,
-                          ctx.tabs);
-    switch (ctx.nsub) {
-        case 2: return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, 2>, 2, P.total_blocks, ctx, P,
-                                  ctx.tabs);
-        case 4:
-            if constexpr (G != G_F32)
-                return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, 4>, 4, P.total_blocks, ctx, P,
-                                  ctx.tabs);
-            [[fallthrough]];
-        default: return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, 3>, 3, P.total_blocks, ctx, P,
-                                   ctx.tabs);
-    }
+    const int subt = ctx.subt ? ctx.subt : (Q8_GDT == G_F32 ? 256 : 128);
+    return subt == 128 ? launch_kind_t<KIND, MAXT, 128>(P, ctx) : launch_kind_t<KIND, MAXT, 256>(P, ctx);
 }
 
 template <int MAXT>
