@@ -18,8 +18,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-ADAM, ADAMW, MOMENTUM = 0, 1, 2
-KINDS = {"adam": ADAM, "adamw": ADAMW, "momentum": MOMENTUM}
+ADAM, ADAMW, MOMENTUM, LAMB, LARS = 0, 1, 2, 3, 4
+KINDS = {"adam": ADAM, "adamw": ADAMW, "momentum": MOMENTUM, "lamb": LAMB, "lars": LARS}
 CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-pthread"]
 
 
@@ -62,6 +62,10 @@ def lib():
                                              ctypes.POINTER(_HParams), i64]
         l.oracle_optim8bit_step.argtypes = [ctypes.c_int, f32p, f32p, u8p, u8p, f32p, f32p, i64, i64,
                                             ctypes.POINTER(_HParams), i64, ctypes.c_int]
+        l.oracle_optim32bit_layerwise_step.argtypes = [ctypes.c_int, f32p, f32p, f32p, f32p, i64,
+                                                       ctypes.POINTER(_HParams), ctypes.c_double, i64, f32p]
+        l.oracle_optim8bit_layerwise_step.argtypes = [ctypes.c_int, f32p, f32p, u8p, u8p, f32p, f32p, i64, i64,
+                                                      ctypes.POINTER(_HParams), ctypes.c_double, i64, f32p]
         _lib = l
     return _lib
 
@@ -165,3 +169,48 @@ def optim8bit_step(kind, p, g, s1, s2, absmax1, absmax2, *, lr, beta1=0.9, beta2
                                      p.size, blocksize, ctypes.byref(hp), int(step), int(nthreads))
     if rc != 0:
         raise ValueError("invalid arguments")
+
+
+def optim32bit_layerwise_step(kind, p, g, m, r, *, lr, beta1=0.9, beta2=0.999, eps=1e-6, weight_decay=0.0,
+                              bias_correction=True, step=1, trust_coefficient=0.001):
+    """In-place 32-bit LAMB / LARS step over ONE tensor (readings L1-L4 in oracle.c).  p, m, r
+    float32 (r LAMB only).  Returns the fp32 per-tensor scale RN(lr*trust ratio)."""
+    kind = KINDS.get(kind, kind)
+    for a in (p, m) + ((r,) if kind == LAMB else ()):
+        assert a.dtype == np.float32 and a.flags.c_contiguous
+    g = _f32(g)
+    if r is None:
+        r = np.zeros(1, np.float32)
+    hp = _hp(lr, beta1, beta2, eps, weight_decay, bias_correction)
+    out = np.zeros(1, np.float32)
+    rc = lib().oracle_optim32bit_layerwise_step(kind, _ptr(p, ctypes.c_float), _ptr(g, ctypes.c_float),
+                                                _ptr(m, ctypes.c_float), _ptr(r, ctypes.c_float), p.size,
+                                                ctypes.byref(hp), float(trust_coefficient), int(step),
+                                                _ptr(out, ctypes.c_float))
+    if rc != 0:
+        raise ValueError("invalid arguments")
+    return out[0]
+
+
+def optim8bit_layerwise_step(kind, p, g, s1, s2, absmax1, absmax2, *, lr, beta1=0.9, beta2=0.999, eps=1e-6,
+                             weight_decay=0.0, bias_correction=True, step=1, trust_coefficient=0.001,
+                             blocksize=2048):
+    """In-place 8-bit LAMB / LARS step over ONE tensor (s2/absmax2 LAMB only).  Returns the
+    fp32 per-tensor scale."""
+    kind = KINDS.get(kind, kind)
+    for a, dt in ((p, np.float32), (s1, np.uint8), (absmax1, np.float32)):
+        assert a.dtype == dt and a.flags.c_contiguous
+    g = _f32(g)
+    if s2 is None:
+        s2 = np.zeros(1, np.uint8)
+        absmax2 = np.zeros(1, np.float32)
+    hp = _hp(lr, beta1, beta2, eps, weight_decay, bias_correction)
+    out = np.zeros(1, np.float32)
+    rc = lib().oracle_optim8bit_layerwise_step(kind, _ptr(p, ctypes.c_float), _ptr(g, ctypes.c_float),
+                                               _ptr(s1, ctypes.c_uint8), _ptr(s2, ctypes.c_uint8),
+                                               _ptr(absmax1, ctypes.c_float), _ptr(absmax2, ctypes.c_float),
+                                               p.size, blocksize, ctypes.byref(hp), float(trust_coefficient),
+                                               int(step), _ptr(out, ctypes.c_float))
+    if rc != 0:
+        raise ValueError("invalid arguments")
+    return out[0]

@@ -29,6 +29,14 @@
  *   oracle_optim8bit_step      pinned: == 32-bit step + explicit block quantize
  *                              (bit-exact), 8-bit vs 32-bit within quantization
  *                              error over 10 steps
+ *   oracle_optim32bit_layerwise_step  (8-bit LAMB / LARS, T5 P:366-367; readings L1-L4)
+ *                              pinned: LAMB states == Adam states (bit-exact); LAMB
+ *                              p against the unfolded textbook form in float64 and
+ *                              |dw| = lr*|w| closed forms; LARS == torch.optim.SGD on
+ *                              the trust-scaled gradient (bit-exact), |dw| closed form
+ *   oracle_optim8bit_layerwise_step   pinned: == dequantize -> 32-bit layer-wise step
+ *                              -> block quantize (bit-exact), 8-bit vs 32-bit within
+ *                              quantization error
  */
 #include <math.h>
 #include <pthread.h>
@@ -39,6 +47,8 @@
 #define ORACLE_ADAM 0
 #define ORACLE_ADAMW 1
 #define ORACLE_MOMENTUM 2
+#define ORACLE_LAMB 3
+#define ORACLE_LARS 4
 
 typedef struct {
     double lr;            /* alpha,  Eq.1/Eq.2 */
@@ -334,4 +344,101 @@ int oracle_optim8bit_step(int kind, float* p, const float* g, uint8_t* s1, uint8
     step_blocks(&jobs[0]);
     for (int t = 1; t < nthreads; t++) pthread_join(th[t], NULL);
     return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* 6. Layer-wise (trust-ratio) optimizers: 8-bit LAMB and LARS (T5)  */
+/* ------------------------------------------------------------------------- */
+/*
+ * The paper benchmarks 8-bit LAMB and LARS (T5) but prints no formula for them; they are
+ * the textbook algorithms with their states quantized exactly like Adam's / Momentum's
+ * (S3: dequantize -> 32-bit update -> requantize).  Readings (L1-L4):
+ *
+ * L1 LAMB (You et al. 2020, "Large Batch Optimization for Deep Learning", Alg. 2), per
+ *    tensor ("layer"):  m, r as Eq.2 (G9 order, no L2 term in g);
+ *      d = m / (sqrt(r) + eps_hat);   u = c*d + wd*w   with c = sqrt(1-b2^t)/(1-b1^t)
+ *      (the folded bias correction of G8; c = 1 without it);
+ *      ratio = ||w|| / ||u|| if both norms > 0, else 1;   w = w - RN(lr*ratio) * u.
+ * L2 LARS (You, Gitman & Ginsburg 2017, "Large Batch Training of Convolutional
+ *    Networks", Alg. 1), per tensor, momentum state v (signed table):
+ *      local = eta * ||w|| / (||g|| + wd*||w||) if ||w|| > 0 and ||g|| > 0, else 1;
+ *      v = beta1*v + RN(lr*local) * (g + wd*w);   w = w - v.
+ * L3 Norms: ||x|| = sqrt(sum_i x_i^2) over the whole tensor, squares and sum in binary64
+ *    (sequential here), ratio / local in binary64, the per-tensor scale rounded once to
+ *    binary32.  Norms use the PRE-update w (and, LAMB, the fp32 post-update states).
+ * L4 Each fp32 operator above is one IEEE RN operation in the written order (as G9).
+ */
+
+static double sum_squares(const float* x, int64_t n) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; i++) s += (double)x[i] * (double)x[i];
+    return s;
+}
+
+/* 32-bit layer-wise step over ONE tensor (the layer).  m, r fp32 states (r LAMB only);
+ * *scale_out (may be NULL) receives the fp32 per-tensor scale RN(lr*ratio) / RN(lr*local). */
+int oracle_optim32bit_layerwise_step(int kind, float* p, const float* g, float* m, float* r, int64_t n,
+                                     const oracle_hparams* hp, double trust_coeff, int64_t step, float* scale_out) {
+    if ((kind != ORACLE_LAMB && kind != ORACLE_LARS) || n < 0 || step < 1) return -1;
+    const float beta1 = (float)hp->beta1, wd = (float)hp->weight_decay;
+    float a;
+    if (kind == ORACLE_LAMB) {
+        const float beta2 = (float)hp->beta2;
+        const float omb1 = (float)(1.0 - hp->beta1), omb2 = (float)(1.0 - hp->beta2);
+        float c = 1.0f, eps_hat = (float)hp->eps;
+        if (hp->bias_correction) {
+            double bc1 = 1.0 - pow(hp->beta1, (double)step);
+            double bc2 = 1.0 - pow(hp->beta2, (double)step);
+            c = (float)(sqrt(bc2) / bc1);
+            eps_hat = (float)(hp->eps * sqrt(bc2));
+        }
+        float* u = (float*)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
+        for (int64_t i = 0; i < n; i++) {
+            m[i] = beta1 * m[i] + omb1 * g[i];                 /* Eq.2 state 1 */
+            r[i] = beta2 * r[i] + omb2 * (g[i] * g[i]);        /* Eq.2 state 2 */
+            float d = m[i] / (sqrtf(r[i]) + eps_hat);
+            u[i] = c * d + wd * p[i];                          /* LAMB update direction */
+        }
+        double wn = sqrt(sum_squares(p, n)), un = sqrt(sum_squares(u, n));
+        double ratio = (wn > 0.0 && un > 0.0) ? wn / un : 1.0; /* trust ratio */
+        a = (float)(hp->lr * ratio);
+        for (int64_t i = 0; i < n; i++) p[i] = p[i] - a * u[i];
+        free(u);
+    } else {
+        double wn = sqrt(sum_squares(p, n)), gn = sqrt(sum_squares(g, n));
+        double local = (wn > 0.0 && gn > 0.0) ? trust_coeff * wn / (gn + hp->weight_decay * wn) : 1.0;
+        a = (float)(hp->lr * local);
+        for (int64_t i = 0; i < n; i++) {
+            float t = g[i] + wd * p[i];
+            t = a * t;
+            m[i] = beta1 * m[i] + t;                           /* v = beta1 v + lr*local*(g + wd w) */
+            p[i] = p[i] - m[i];
+        }
+    }
+    if (scale_out) *scale_out = a;
+    return 0;
+}
+
+/* 8-bit layer-wise step over ONE tensor: dequantize all states, the 32-bit layer-wise
+ * step above, block-wise requantization of the new states (Eq.4); s1 signed, s2 unsigned
+ * (LAMB only, G14). */
+int oracle_optim8bit_layerwise_step(int kind, float* p, const float* g, uint8_t* s1, uint8_t* s2, float* absmax1,
+                                    float* absmax2, int64_t n, int64_t B, const oracle_hparams* hp, double trust_coeff,
+                                    int64_t step, float* scale_out) {
+    if ((kind != ORACLE_LAMB && kind != ORACLE_LARS) || n < 0 || B < 1 || step < 1) return -1;
+    float Qs[256], Qu[256];
+    if (oracle_dynamic_codebook(1, Qs) != 0 || oracle_dynamic_codebook(0, Qu) != 0) return -1;
+    size_t bytes = sizeof(float) * (size_t)(n > 0 ? n : 1);
+    float* m = (float*)malloc(bytes);
+    float* r = (float*)malloc(bytes);
+    oracle_dequantize_blockwise(Qs, s1, absmax1, n, B, m);
+    if (kind == ORACLE_LAMB) oracle_dequantize_blockwise(Qu, s2, absmax2, n, B, r);
+    int rc = oracle_optim32bit_layerwise_step(kind, p, g, m, r, n, hp, trust_coeff, step, scale_out);
+    if (rc == 0) {
+        oracle_quantize_blockwise(Qs, m, n, B, absmax1, s1);
+        if (kind == ORACLE_LAMB) oracle_quantize_blockwise(Qu, r, n, B, absmax2, s2);
+    }
+    free(m);
+    free(r);
+    return rc;
 }

@@ -87,6 +87,11 @@ HPARAMS = {
     "adam_paper": dict(lr=0.0163, beta1=0.9, beta2=0.995, eps=1e-7, weight_decay=0.0, bias_correction=True),
     "adamw": dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, bias_correction=True),
     "momentum": dict(lr=0.1, beta1=0.9, beta2=0.0, eps=1e-8, weight_decay=1e-4, bias_correction=False),
+    # layer-wise optimizers of T5: LAMB (You et al. 2020 defaults), LARS (You et al.
+    # 2017: trust coefficient eta = 0.001, wd 5e-4, momentum 0.9)
+    "lamb": dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-6, weight_decay=0.01, bias_correction=True),
+    "lars": dict(lr=0.1, beta1=0.9, beta2=0.0, eps=1e-8, weight_decay=5e-4, bias_correction=False,
+                 trust_coefficient=0.001),
 }
 
 
