@@ -41,18 +41,20 @@ typedef enum {
 } q8_status;
 
 typedef enum { Q8_F32 = 0, Q8_F16 = 1, Q8_BF16 = 2 } q8_dtype;          /* gradient dtype (G13) */
-typedef enum { Q8_ADAM = 0, Q8_ADAMW = 1, Q8_MOMENTUM = 2 } q8_kind;    /* Eq.2, AdamW, Eq.1 */
+/* Eq.2, AdamW, Eq.1; the layer-wise LAMB and LARS of T5 are taken only by
+ * q8_optim8bit_step_layerwise */
+typedef enum { Q8_ADAM = 0, Q8_ADAMW = 1, Q8_MOMENTUM = 2, Q8_LAMB = 3, Q8_LARS = 4 } q8_kind;
 
 /* Optimizer hyper-parameters (host struct, doubles; every derived fp32 scalar is computed
  * in double and rounded once, G8-G10).
  *   lr            alpha of Eq.1/Eq.2, >= 0
- *   beta1         beta_1 of Eq.2; the momentum beta of Eq.1 for Q8_MOMENTUM; in [0, 1)
- *   beta2         beta_2 of Eq.2, in [0, 1) (ignored by Q8_MOMENTUM)
- *   eps           epsilon of Eq.2, > 0 (ignored by Q8_MOMENTUM)
+ *   beta1         beta_1 of Eq.2; the momentum beta of Eq.1 for Q8_MOMENTUM / Q8_LARS; in [0, 1)
+ *   beta2         beta_2 of Eq.2, in [0, 1) (ignored by Q8_MOMENTUM / Q8_LARS)
+ *   eps           epsilon of Eq.2, > 0 (ignored by Q8_MOMENTUM / Q8_LARS)
  *   weight_decay  >= 0.  Q8_ADAMW: decoupled, w *= (1 - lr*wd) before the update.
- *                 Q8_ADAM / Q8_MOMENTUM: L2, g += wd*w (G10)
+ *                 Q8_ADAM / Q8_MOMENTUM: L2, g += wd*w (G10).  Q8_LAMB / Q8_LARS: L1 / L2
  *   bias_correction  0/1: Kingma & Ba's folded correction alpha_t, eps_hat (G8);
- *                 ignored by Q8_MOMENTUM */
+ *                 ignored by Q8_MOMENTUM / Q8_LARS */
 typedef struct {
     double lr, beta1, beta2, eps, weight_decay;
     int32_t bias_correction;
@@ -172,6 +174,36 @@ typedef struct {
  * q8_optim8bit_step_multi. */
 q8_status q8_optim32bit_step_multi(q8_kind kind, q8_dtype g_dtype, const q8_tensor32* tensors_host,
                                    int32_t num_tensors, const q8_hparams* hp, int64_t step, void* stream);
+
+/* Layer-wise (trust-ratio) 8-bit optimizers: 8-bit LAMB and LARS, which the paper benchmarks
+ * (T5) without printing their formulas; readings L1-L4, per tensor
+ * ("layer") t of tensors_host[num_tensors]:
+ *   Q8_LAMB (You et al. 2020, Alg. 2): states m, r as Eq.2 (s1 signed, s2 unsigned),
+ *            u = c * m/(sqrt(r) + eps_hat) + wd*w  (c = sqrt(1-b2^t)/(1-b1^t), G8),
+ *            w -= RN(lr * ||w||/||u||) * u  (ratio 1 when either norm is 0)
+ *   Q8_LARS (You et al. 2017, Alg. 1): momentum state v (s1 signed; s2/absmax2 unused),
+ *            v = beta1*v + RN(lr * eta*||w||/(||g|| + wd*||w||)) * (g + wd*w),  w -= v
+ *            (the factor is lr when either norm is 0); eta = trust_coefficient > 0
+ * Norms are over the whole tensor, of the PRE-update w (and of u from the fp32 post-update
+ * states), accumulated in binary64; the per-tensor scale is rounded once to fp32 (L3).  States
+ * are dequantized / requantized block-wise exactly as in q8_optim8bit_step.
+ * Three stream-ordered launches per chunk of Q8_MAX_TENSORS_PER_LAUNCH tensors: a norms pass
+ * (reads w, g and, LAMB, the states), a per-tensor scale pass, the fused step.
+ *   workspace_dev  device scratch of at least q8_layerwise_workspace_bytes(tensors, n) bytes,
+ *                  16-B aligned, caller-owned; must not be used by another call until this one
+ *                  completes on `stream`.  On completion its first 4*num_tensors bytes hold each
+ *                  tensor's fp32 scale (float scale[i] for tensors_host[i]; lr for empty tensors)
+ *                  -- the trust ratio times lr, a diagnostic output.
+ * Other arguments, alignment and errors as q8_optim8bit_step_multi; INVALID also for a kind
+ * other than LAMB/LARS, trust_coefficient <= 0 (LARS) or a too-small workspace. */
+q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_tensor* tensors_host,
+                                      int32_t num_tensors, int32_t blocksize, const q8_hparams* hp,
+                                      double trust_coefficient, int64_t step, void* workspace_dev,
+                                      int64_t workspace_bytes, void* stream);
+
+/* Bytes of workspace q8_optim8bit_step_layerwise needs for these tensors (host function): 4 per
+ * tensor (rounded up to 16) + 16 per 2048-block of the largest launch chunk.  -1 on bad input. */
+int64_t q8_layerwise_workspace_bytes(const q8_tensor* tensors_host, int32_t num_tensors);
 
 /* Thread-local description of the last error ("" after success). */
 const char* q8_last_error(void);

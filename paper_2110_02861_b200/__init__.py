@@ -16,10 +16,11 @@ __all__ = [
     "dequantize_blockwise", "hparams", "nblocks", "optim8bit_step", "optim8bit_step_multi", "quantize_blockwise",
     "quantize_blockwise_dynamic", "version",
 ]
-from ._binding import optim32bit_step_multi  # noqa: E402
+from ._binding import layerwise_workspace_bytes, optim8bit_step_layerwise, optim32bit_step_multi  # noqa: E402
 from .modules import StableEmbedding  # noqa: E402
-from .optim import Adam8bit, AdamW8bit, Momentum8bit, state_bytes  # noqa: E402
+from .optim import LAMB8bit, LARS8bit, Adam8bit, AdamW8bit, Momentum8bit, state_bytes  # noqa: E402
 from .zero import Zero1Optimizer8bit, padded_numel, shard_range  # noqa: E402
 
-__all__ += ["optim32bit_step_multi", "StableEmbedding", "Adam8bit", "AdamW8bit", "Momentum8bit", "state_bytes", "Zero1Optimizer8bit", "padded_numel",
+__all__ += ["layerwise_workspace_bytes", "optim8bit_step_layerwise", "LAMB8bit", "LARS8bit",
+            "optim32bit_step_multi", "StableEmbedding", "Adam8bit", "AdamW8bit", "Momentum8bit", "state_bytes", "Zero1Optimizer8bit", "padded_numel",
             "shard_range"]

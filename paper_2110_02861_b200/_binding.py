@@ -14,17 +14,18 @@ LIB_PATH = os.environ.get("Q8_LIB_PATH") or os.path.join(_HERE, "libq8.so")
 
 Q8_OK, Q8_ERR_INVALID, Q8_ERR_UNSUPPORTED, Q8_ERR_CUDA = 0, -1, -2, -3
 Q8_F32, Q8_F16, Q8_BF16 = 0, 1, 2
-Q8_ADAM, Q8_ADAMW, Q8_MOMENTUM = 0, 1, 2
+Q8_ADAM, Q8_ADAMW, Q8_MOMENTUM, Q8_LAMB, Q8_LARS = 0, 1, 2, 3, 4
 MAX_TENSORS_PER_LAUNCH = 384
 BLOCKSIZE = 2048
 
-KINDS = {"adam": Q8_ADAM, "adamw": Q8_ADAMW, "momentum": Q8_MOMENTUM}
+KINDS = {"adam": Q8_ADAM, "adamw": Q8_ADAMW, "momentum": Q8_MOMENTUM, "lamb": Q8_LAMB, "lars": Q8_LARS}
 GDTYPES = {torch.float32: Q8_F32, torch.float16: Q8_F16, torch.bfloat16: Q8_BF16}
 
 EXPORTS = ("q8_create_dynamic_codebook", "q8_create_linear_codebook", "q8_quantize_blockwise",
            "q8_quantize_blockwise_dynamic", "q8_dequantize_blockwise", "q8_quantize_tensorwise",
            "q8_dequantize_tensorwise",
-           "q8_optim8bit_step", "q8_optim8bit_step_multi", "q8_optim32bit_step_multi", "q8_last_error", "q8_version")
+           "q8_optim8bit_step", "q8_optim8bit_step_multi", "q8_optim32bit_step_multi",
+           "q8_optim8bit_step_layerwise", "q8_layerwise_workspace_bytes", "q8_last_error", "q8_version")
 
 
 class Q8Error(RuntimeError):
@@ -65,8 +66,12 @@ def _load():
                                             ctypes.POINTER(HParams), i64, vp]
     lib.q8_optim32bit_step_multi.argtypes = [i32, i32, ctypes.POINTER(TensorDesc32), i32, ctypes.POINTER(HParams),
                                              i64, vp]
+    lib.q8_optim8bit_step_layerwise.argtypes = [i32, i32, ctypes.POINTER(TensorDesc), i32, i32,
+                                                ctypes.POINTER(HParams), ctypes.c_double, i64, vp, i64, vp]
+    lib.q8_layerwise_workspace_bytes.argtypes = [ctypes.POINTER(TensorDesc), i32]
     for f in EXPORTS[:-2]:
         getattr(lib, f).restype = ctypes.c_int
+    lib.q8_layerwise_workspace_bytes.restype = i64
     lib.q8_last_error.restype = ctypes.c_char_p
     lib.q8_version.restype = ctypes.c_char_p
     return lib
@@ -201,7 +206,7 @@ def optim8bit_step(kind, p, g, s1, s2, absmax1, absmax2, *, lr, beta1=0.9, beta2
     """One fused 8-bit step on a single flat tensor (in place)."""
     kind = KINDS.get(kind, kind)
     n = p.numel()
-    if g.numel() != n or s1.numel() != n or (kind != Q8_MOMENTUM and s2.numel() != n):
+    if g.numel() != n or s1.numel() != n or (kind in (Q8_ADAM, Q8_ADAMW) and s2.numel() != n):
         raise ValueError("size mismatch")
     if g.dtype not in GDTYPES:
         raise ValueError(f"unsupported gradient dtype {g.dtype}")
@@ -275,3 +280,35 @@ def optim32bit_step_multi(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1e-8
         hp = hparams(lr, beta1, beta2, eps, weight_decay, bias_correction)
     _check(lib.q8_optim32bit_step_multi(kind, gd, arr, len(entries), ctypes.byref(hp), int(step),
                                         _stream(entries[0][0].device)))
+
+
+def layerwise_workspace_bytes(tensors) -> int:
+    tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
+    nb = lib.q8_layerwise_workspace_bytes(tl.arr, tl.count)
+    if nb < 0:
+        raise ValueError("invalid tensor list")
+    return nb
+
+
+def optim8bit_step_layerwise(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1e-6, weight_decay=0.0,
+                             bias_correction=True, step=1, trust_coefficient=0.001, blocksize=BLOCKSIZE,
+                             workspace: torch.Tensor | None = None, hp: HParams | None = None) -> torch.Tensor:
+    """One 8-bit LAMB / LARS step over many tensors (each tensor is one layer: its own trust
+    ratio).  entries as optim8bit_step_multi (s2/absmax2 None for LARS).  Returns the float32
+    per-tensor scales RN(lr * ratio) (a view into the workspace, valid until its next use)."""
+    kind = KINDS.get(kind, kind)
+    tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
+    if tl.count == 0:
+        return torch.empty(0, dtype=torch.float32)
+    need = lib.q8_layerwise_workspace_bytes(tl.arr, tl.count)
+    if need < 0:
+        raise ValueError("invalid tensor list")
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=tl.device)
+    if hp is None:
+        hp = hparams(lr, beta1, beta2, eps, weight_decay, bias_correction)
+    _check(lib.q8_optim8bit_step_layerwise(kind, tl.gdtype, tl.arr, tl.count, blocksize, ctypes.byref(hp),
+                                           float(trust_coefficient), int(step), _dev_ptr(workspace, torch.uint8,
+                                                                                         "workspace"),
+                                           workspace.numel(), _stream(tl.device)))
+    return workspace[:4 * tl.count].view(torch.float32)

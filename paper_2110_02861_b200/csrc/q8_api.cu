@@ -116,12 +116,13 @@ int64_t grid_for(const DeviceState* d, int occ, int64_t nblocks) {
 // ---------------------------------------------------------------- hparams
 q8_status validate_hparams(q8_kind kind, const q8_hparams* hp, int64_t step) {
     if (!hp) return fail(Q8_ERR_INVALID, "hparams is NULL");
-    if (kind != Q8_ADAM && kind != Q8_ADAMW && kind != Q8_MOMENTUM) return fail(Q8_ERR_INVALID, "bad kind %d", kind);
+    if (kind != Q8_ADAM && kind != Q8_ADAMW && kind != Q8_MOMENTUM && kind != Q8_LAMB && kind != Q8_LARS)
+        return fail(Q8_ERR_INVALID, "bad kind %d", kind);
     if (!(hp->lr >= 0.0) || !std::isfinite(hp->lr)) return fail(Q8_ERR_INVALID, "lr must be finite and >= 0");
     if (!(hp->beta1 >= 0.0 && hp->beta1 < 1.0)) return fail(Q8_ERR_INVALID, "beta1 must be in [0, 1)");
     if (!(hp->weight_decay >= 0.0) || !std::isfinite(hp->weight_decay))
         return fail(Q8_ERR_INVALID, "weight_decay must be finite and >= 0");
-    if (kind != Q8_MOMENTUM) {
+    if (q8::two_states(kind)) {
         if (!(hp->beta2 >= 0.0 && hp->beta2 < 1.0)) return fail(Q8_ERR_INVALID, "beta2 must be in [0, 1)");
         if (!(hp->eps > 0.0) || !std::isfinite(hp->eps)) return fail(Q8_ERR_INVALID, "eps must be finite and > 0");
     }
@@ -129,8 +130,15 @@ q8_status validate_hparams(q8_kind kind, const q8_hparams* hp, int64_t step) {
     return Q8_OK;
 }
 
-// fp32 scalars of the update, computed in double and rounded once (G8-G10).
-q8::StepScalars make_scalars(const q8_hparams* hp, int64_t step) {
+// Element-wise entry points take the Adam family and Momentum only.
+q8_status reject_layerwise(q8_kind kind) {
+    if (kind == Q8_LAMB || kind == Q8_LARS)
+        return fail(Q8_ERR_INVALID, "kind %d is layer-wise: use q8_optim8bit_step_layerwise", kind);
+    return Q8_OK;
+}
+
+// fp32 scalars of the update, computed in double and rounded once (G8-G10; LAMB L1).
+q8::StepScalars make_scalars(const q8_hparams* hp, int64_t step, q8_kind kind = Q8_ADAM) {
     q8::StepScalars s;
     s.lr = static_cast<float>(hp->lr);
     s.beta1 = static_cast<float>(hp->beta1);
@@ -150,6 +158,13 @@ q8::StepScalars make_scalars(const q8_hparams* hp, int64_t step) {
     }
     s.wd = static_cast<float>(hp->weight_decay);
     s.decay = static_cast<float>(1.0 - hp->lr * hp->weight_decay);
+    if (kind == Q8_LAMB) {
+        // LAMB: u = c*d + wd*w with the bias-correction factor c alone; lr enters the trust scale
+        s.step_size = hp->bias_correction ? static_cast<float>(
+                                                std::sqrt(1.0 - std::pow(hp->beta2, static_cast<double>(step))) /
+                                                (1.0 - std::pow(hp->beta1, static_cast<double>(step))))
+                                          : 1.0f;
+    }
     s.fast_div = (s.eps_hat >= 0x1p-40f && std::isfinite(s.eps_hat)) ? 1 : 0;
     return s;
 }
@@ -157,7 +172,7 @@ q8::StepScalars make_scalars(const q8_hparams* hp, int64_t step) {
 q8_status validate_tensor(q8_kind kind, q8_dtype gdt, const q8_tensor& t, int idx) {
     if (t.n < 0) return fail(Q8_ERR_INVALID, "tensor %d: n < 0", idx);
     if (t.n == 0) return Q8_OK;
-    const bool two = kind != Q8_MOMENTUM;
+    const bool two = q8::two_states(kind);
     if (!t.p || !t.g || !t.s1 || !t.absmax1 || (two && (!t.s2 || !t.absmax2)))
         return fail(Q8_ERR_INVALID, "tensor %d: NULL buffer with n > 0", idx);
     if (!aligned(t.p, 16)) return fail(Q8_ERR_INVALID, "tensor %d: p not 16-byte aligned", idx);
@@ -373,6 +388,7 @@ q8_status q8_dequantize_blockwise(const float* code_dev, const uint8_t* codes_de
 q8_status q8_optim8bit_step(q8_kind kind, float* p, const void* g, q8_dtype g_dtype, uint8_t* s1, uint8_t* s2,
                             float* absmax1, float* absmax2, int64_t n, int32_t blocksize, const q8_hparams* hp,
                             int64_t step, void* stream) {
+    if (q8_status s = reject_layerwise(kind); s != Q8_OK) return s;
     if (q8_status s = check_common(g_dtype, blocksize); s != Q8_OK) return s;
     if (q8_status s = validate_hparams(kind, hp, step); s != Q8_OK) return s;
     q8_tensor t{p, g, s1, s2, absmax1, absmax2, n};
@@ -382,6 +398,7 @@ q8_status q8_optim8bit_step(q8_kind kind, float* p, const void* g, q8_dtype g_dt
     if (q8_status s = device_state(&d); s != Q8_OK) return s;
     q8::StepParams<1> P;
     P.s = make_scalars(hp, step);
+    P.scale = nullptr;
     P.num_tensors = 1;
     P.block_start[0] = 0;
     P.total_blocks = P.block_start[1] = (n + q8::kBlock - 1) / q8::kBlock;
@@ -392,6 +409,7 @@ q8_status q8_optim8bit_step(q8_kind kind, float* p, const void* g, q8_dtype g_dt
 
 q8_status q8_optim8bit_step_multi(q8_kind kind, q8_dtype g_dtype, const q8_tensor* tensors_host, int32_t num_tensors,
                                   int32_t blocksize, const q8_hparams* hp, int64_t step, void* stream) {
+    if (q8_status s = reject_layerwise(kind); s != Q8_OK) return s;
     if (q8_status s = check_common(g_dtype, blocksize); s != Q8_OK) return s;
     if (q8_status s = validate_hparams(kind, hp, step); s != Q8_OK) return s;
     if (num_tensors < 0) return fail(Q8_ERR_INVALID, "num_tensors < 0");
@@ -403,6 +421,7 @@ q8_status q8_optim8bit_step_multi(q8_kind kind, q8_dtype g_dtype, const q8_tenso
     constexpr int MAXT = Q8_MAX_TENSORS_PER_LAUNCH;
     static thread_local q8::StepParams<MAXT> P;  // ~24 KB; kernel parameter (copied at launch)
     P.s = make_scalars(hp, step);
+    P.scale = nullptr;
     int i = 0;
     while (i < num_tensors) {
         int k = 0;
@@ -464,6 +483,7 @@ extern "C" {
 
 q8_status q8_optim32bit_step_multi(q8_kind kind, q8_dtype g_dtype, const q8_tensor32* tensors_host,
                                    int32_t num_tensors, const q8_hparams* hp, int64_t step, void* stream) {
+    if (q8_status s = reject_layerwise(kind); s != Q8_OK) return s;
     if (q8_status s = check_common(g_dtype, q8::kBlock); s != Q8_OK) return s;
     if (q8_status s = validate_hparams(kind, hp, step); s != Q8_OK) return s;
     if (num_tensors < 0) return fail(Q8_ERR_INVALID, "num_tensors < 0");
@@ -475,6 +495,7 @@ q8_status q8_optim32bit_step_multi(q8_kind kind, q8_dtype g_dtype, const q8_tens
     constexpr int MAXT = Q8_MAX_TENSORS_PER_LAUNCH;
     static thread_local q8::StepParams<MAXT> P;
     P.s = make_scalars(hp, step);
+    P.scale = nullptr;
     int i = 0;
     while (i < num_tensors) {
         int k = 0;
@@ -494,6 +515,95 @@ q8_status q8_optim32bit_step_multi(q8_kind kind, q8_dtype g_dtype, const q8_tens
         P.total_blocks = blocks;
         if (q8_status s = launch_step32<MAXT>(kind, g_dtype, P, d, static_cast<cudaStream_t>(stream)); s != Q8_OK)
             return s;
+    }
+    return ok();
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- layer-wise step (LAMB / LARS)
+
+namespace {
+
+constexpr int kLwChunk = Q8_MAX_TENSORS_PER_LAUNCH;
+
+// Workspace layout: float scale[num_tensors] (rounded up to 16 B), then double2 partial[] sized
+// for the largest chunk of kLwChunk consecutive tensors.
+int64_t lw_scale_bytes(int32_t num_tensors) { return (static_cast<int64_t>(num_tensors) * 4 + 15) / 16 * 16; }
+
+int64_t lw_partial_blocks(const q8_tensor* t, int32_t num_tensors) {
+    int64_t best = 0;
+    for (int32_t c = 0; c < num_tensors; c += kLwChunk) {
+        int64_t blocks = 0;
+        for (int32_t i = c; i < std::min(num_tensors, c + kLwChunk); ++i) blocks += (t[i].n + q8::kBlock - 1) / q8::kBlock;
+        best = std::max(best, blocks);
+    }
+    return best;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t q8_layerwise_workspace_bytes(const q8_tensor* tensors_host, int32_t num_tensors) {
+    if (num_tensors < 0 || (num_tensors > 0 && !tensors_host)) return -1;
+    for (int32_t i = 0; i < num_tensors; ++i)
+        if (tensors_host[i].n < 0) return -1;
+    return lw_scale_bytes(num_tensors) + 16 * lw_partial_blocks(tensors_host, num_tensors);
+}
+
+q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_tensor* tensors_host,
+                                      int32_t num_tensors, int32_t blocksize, const q8_hparams* hp,
+                                      double trust_coefficient, int64_t step, void* workspace_dev,
+                                      int64_t workspace_bytes, void* stream) {
+    if (kind != Q8_LAMB && kind != Q8_LARS) return fail(Q8_ERR_INVALID, "kind %d is not layer-wise (LAMB/LARS)", kind);
+    if (q8_status s = check_common(g_dtype, blocksize); s != Q8_OK) return s;
+    if (q8_status s = validate_hparams(kind, hp, step); s != Q8_OK) return s;
+    if (kind == Q8_LARS && !(trust_coefficient > 0.0 && std::isfinite(trust_coefficient)))
+        return fail(Q8_ERR_INVALID, "trust_coefficient must be finite and > 0");
+    if (num_tensors < 0) return fail(Q8_ERR_INVALID, "num_tensors < 0");
+    if (num_tensors > 0 && !tensors_host) return fail(Q8_ERR_INVALID, "tensors_host is NULL");
+    for (int i = 0; i < num_tensors; ++i)
+        if (q8_status s = validate_tensor(kind, g_dtype, tensors_host[i], i); s != Q8_OK) return s;
+    if (num_tensors == 0) return ok();
+    const int64_t need = q8_layerwise_workspace_bytes(tensors_host, num_tensors);
+    if (!workspace_dev || !aligned(workspace_dev, 16))
+        return fail(Q8_ERR_INVALID, "workspace must be a non-NULL 16-byte aligned device buffer");
+    if (workspace_bytes < need)
+        return fail(Q8_ERR_INVALID, "workspace too small: %lld < %lld bytes", static_cast<long long>(workspace_bytes),
+                    static_cast<long long>(need));
+    DeviceState* d = nullptr;
+    if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    float* scale = static_cast<float*>(workspace_dev);
+    double2* partial = reinterpret_cast<double2*>(static_cast<uint8_t*>(workspace_dev) + lw_scale_bytes(num_tensors));
+    static thread_local q8::StepParams<kLwChunk> P;
+    P.s = make_scalars(hp, step, kind);
+    const q8::LaunchCtx ctx{d->tabs, d->sms, static_cast<cudaStream_t>(stream), q8::SEARCH_BUCKET, 0, 0};
+    for (int32_t c = 0; c < num_tensors; c += kLwChunk) {
+        // every tensor of the chunk keeps its slot (empty ones have no blocks) so that
+        // scale[i] belongs to tensors_host[i]
+        const int k = std::min(num_tensors - c, kLwChunk);
+        int64_t blocks = 0;
+        for (int j = 0; j < k; ++j) {
+            const q8_tensor& t = tensors_host[c + j];
+            P.t[j] = q8::TensorDesc{t.p, t.g, t.s1, t.s2, t.absmax1, t.absmax2, t.n};
+            P.block_start[j] = blocks;
+            blocks += (t.n + q8::kBlock - 1) / q8::kBlock;
+        }
+        P.num_tensors = k;
+        P.block_start[k] = blocks;
+        P.total_blocks = blocks;
+        P.scale = scale + c;
+        cudaError_t e = cudaErrorInvalidValue;
+        switch (g_dtype) {
+            case Q8_F32: e = q8::launch_layerwise_g0(kind, P, ctx, partial, scale + c, hp->lr, trust_coefficient,
+                                                     hp->weight_decay); break;
+            case Q8_F16: e = q8::launch_layerwise_g1(kind, P, ctx, partial, scale + c, hp->lr, trust_coefficient,
+                                                     hp->weight_decay); break;
+            case Q8_BF16: e = q8::launch_layerwise_g2(kind, P, ctx, partial, scale + c, hp->lr, trust_coefficient,
+                                                      hp->weight_decay); break;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "layer-wise step launch");
     }
     return ok();
 }

@@ -26,7 +26,10 @@ constexpr int kVec = 4;            // elements per vector group
 constexpr int kGroups = kBlock / (kThreads * kVec);  // 2 groups per thread
 constexpr int kWarps = kThreads / 32;
 
-enum { KIND_ADAM = 0, KIND_ADAMW = 1, KIND_MOMENTUM = 2 };
+enum { KIND_ADAM = 0, KIND_ADAMW = 1, KIND_MOMENTUM = 2, KIND_LAMB = 3, KIND_LARS = 4 };
+// Kinds with two states (s1 signed, s2 unsigned): the Adam family and LAMB; Momentum and LARS
+// keep one (the momentum buffer, signed table).
+__host__ __device__ constexpr bool two_states(int kind) { return kind != KIND_MOMENTUM && kind != KIND_LARS; }
 enum { G_F32 = 0, G_F16 = 1, G_BF16 = 2 };
 
 // Device-resident immutable tables (built on the host, codebook_host.cpp), as fp32 words:
@@ -65,6 +68,7 @@ struct TensorDesc {
 };
 
 struct StepScalars {       // all computed on the host in double, rounded once (G8-G10)
+    // step_size: alpha_t for Adam/AdamW; for LAMB the bias-correction factor c alone (L1)
     float lr, beta1, beta2, omb1, omb2, step_size, eps_hat, wd, decay;
     int fast_div;          // eps_hat >= 2^-40: the packed sqrt/div fast path may be used
 };
@@ -72,6 +76,7 @@ struct StepScalars {       // all computed on the host in double, rounded once (
 template <int MAXT>
 struct StepParams {
     StepScalars s;
+    const float* scale;             // LAMB / LARS: per-tensor trust scale RN(lr*ratio) (L1-L3)
     int num_tensors;
     int64_t total_blocks;
     int64_t block_start[MAXT + 1];  // prefix sums of per-tensor block counts

@@ -28,6 +28,15 @@ cudaError_t launch_step_g1(int kind, const StepParams<1>* single, const StepPara
 cudaError_t launch_step_g2(int kind, const StepParams<1>* single, const StepParams<kMultiMaxT>* multi,
                            const LaunchCtx& ctx);
 
+// Layer-wise step (LAMB / LARS) for gradient dtype g<N>: norms pass, per-tensor scale pass
+// (writes scale[0 .. P.num_tensors)), fused step; partial holds P.total_blocks entries.
+cudaError_t launch_layerwise_g0(int kind, const StepParams<kMultiMaxT>& P, const LaunchCtx& ctx, double2* partial,
+                                float* scale, double lr, double eta, double wd);
+cudaError_t launch_layerwise_g1(int kind, const StepParams<kMultiMaxT>& P, const LaunchCtx& ctx, double2* partial,
+                                float* scale, double lr, double eta, double wd);
+cudaError_t launch_layerwise_g2(int kind, const StepParams<kMultiMaxT>& P, const LaunchCtx& ctx, double2* partial,
+                                float* scale, double lr, double eta, double wd);
+
 // Opt a kernel into `smem` bytes of dynamic shared memory (once per kernel and thread).
 cudaError_t ensure_smem(const void* fn, int smem);
 

@@ -1,6 +1,9 @@
 // step_inst.cu -- instantiates and launches the fused step kernels for ONE gradient dtype
 // (Q8_GDT = 0 fp32, 1 fp16, 2 bf16); build.py compiles this file once per dtype in parallel.
+#include <algorithm>
+
 #include "q8_launch.h"
+#include "q8_layerwise.cuh"
 #include "q8_step_kernel.cuh"
 
 #ifndef Q8_GDT
@@ -59,6 +62,35 @@ cudaError_t launch_any(int kind, const StepParams<MAXT>& P, const LaunchCtx& ctx
     }
 }
 
+// Layer-wise kinds (LAMB, LARS): norms -> per-tensor scale -> fused step, default configuration.
+template <int KIND>
+cudaError_t launch_layerwise_t(const StepParams<kMultiMaxT>& P, const LaunchCtx& ctx, double2* partial,
+                               float* scale, double lr, double eta, double wd) {
+    constexpr int G = Q8_GDT;
+    constexpr int NS = G == G_F32 ? 3 : 4;
+    constexpr int SUBT = G == G_F32 ? 256 : 128;
+    static int occ = [] {
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, layer_norms_kernel<KIND, G, kMultiMaxT>, kThreads, 0) !=
+                cudaSuccess || o < 1)
+            o = 1;
+        return o;
+    }();
+    if (P.total_blocks == 0) {  // only empty tensors: their scale is still defined (lr)
+        layer_scale_kernel<KIND, kMultiMaxT><<<P.num_tensors, 32, 0, ctx.stream>>>(P, partial, scale, lr, eta, wd);
+        return cudaGetLastError();
+    }
+    const int64_t g1 = std::min<int64_t>(P.total_blocks, static_cast<int64_t>(ctx.sms) * occ);
+    layer_norms_kernel<KIND, G, kMultiMaxT><<<static_cast<unsigned>(g1), kThreads, 0, ctx.stream>>>(P, ctx.tabs, partial);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    layer_scale_kernel<KIND, kMultiMaxT><<<P.num_tensors, 32, 0, ctx.stream>>>(P, partial, scale, lr, eta, wd);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return persistent(optim8bit_step_kernel<KIND, G, kMultiMaxT, SEARCH_BUCKET, NS, SUBT>, NS, SUBT, P.total_blocks,
+                      ctx, P, ctx.tabs);
+}
+
 }  // namespace
 
 #define Q8_CAT2(a, b) a##b
@@ -68,4 +100,13 @@ cudaError_t Q8_CAT(launch_step_g, Q8_GDT)(int kind, const StepParams<1>* single,
     return single ? launch_any<1>(kind, *single, ctx) : launch_any<kMultiMaxT>(kind, *multi, ctx);
 }
 
+}  // namespace q8
+
+namespace q8 {
+cudaError_t Q8_CAT(launch_layerwise_g, Q8_GDT)(int kind, const StepParams<kMultiMaxT>& P, const LaunchCtx& ctx,
+                                               double2* partial, float* scale, double lr, double eta, double wd) {
+    if (kind == KIND_LAMB) return launch_layerwise_t<KIND_LAMB>(P, ctx, partial, scale, lr, eta, wd);
+    if (kind == KIND_LARS) return launch_layerwise_t<KIND_LARS>(P, ctx, partial, scale, lr, eta, wd);
+    return cudaErrorInvalidValue;
+}
 }  // namespace q8

@@ -17,6 +17,9 @@ import torch
 from . import _binding as B
 
 
+_TWO_STATES = ("adam", "adamw", "lamb")
+
+
 class _Optimizer8bit(torch.optim.Optimizer):
     kind = "adam"
 
@@ -41,13 +44,13 @@ class _Optimizer8bit(torch.optim.Optimizer):
             st["step"] = 0
             if bits == 32:
                 st["m"] = torch.zeros(n, dtype=torch.float32, device=p.device)
-                if self.kind != "momentum":
+                if self.kind in _TWO_STATES:
                     st["r"] = torch.zeros(n, dtype=torch.float32, device=p.device)
             else:
                 nb = B.nblocks(n)
                 st["s1"] = torch.zeros(n, dtype=torch.uint8, device=p.device)
                 st["absmax1"] = torch.zeros(nb, dtype=torch.float32, device=p.device)
-                if self.kind != "momentum":
+                if self.kind in _TWO_STATES:
                     st["s2"] = torch.zeros(n, dtype=torch.uint8, device=p.device)
                     st["absmax2"] = torch.zeros(nb, dtype=torch.float32, device=p.device)
         return st
@@ -128,8 +131,76 @@ class Momentum8bit(_Optimizer8bit):
         super().__init__(params, lr, (momentum, 0.0), 1e-8, weight_decay, False)
 
 
+class _LayerwiseOptimizer8bit(_Optimizer8bit):
+    """Layer-wise (trust-ratio) optimizers: every parameter tensor is one layer with its own
+    trust ratio (q8_optim8bit_step_layerwise: norms pass, per-tensor scale, fused step).  The
+    per-tensor scales RN(lr * ratio) of the last step are kept in ``state[p]["trust_scale"]``
+    (a 0-d float32 CUDA tensor)."""
+    trust_coefficient = 0.001
+
+    def __init__(self, params, lr, betas, eps, weight_decay, bias_correction):
+        super().__init__(params, lr, betas, eps, weight_decay, bias_correction)
+        self._workspace = None
+
+    @torch.no_grad()
+    def step(self, closure=None):
+        loss = None
+        if closure is not None:
+            with torch.enable_grad():
+                loss = closure()
+        for group in self.param_groups:
+            buckets = {}
+            for p in group["params"]:
+                if p.grad is None:
+                    continue
+                if p.grad.is_sparse:
+                    raise TypeError("sparse gradients are not supported")
+                if self._bits(p, group) != 8:
+                    raise NotImplementedError("layer-wise 8-bit optimizers keep 8-bit states only")
+                st = self._state_for(p, 8)
+                st["step"] += 1
+                g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
+                buckets.setdefault((g.dtype, st["step"]), []).append(
+                    (p, g, st["s1"], st.get("s2"), st["absmax1"], st.get("absmax2")))
+            b1, b2 = group["betas"]
+            hp = B.hparams(group["lr"], b1, b2, group["eps"], group["weight_decay"], group["bias_correction"])
+            eta = group.get("trust_coefficient", self.trust_coefficient)
+            for (_, step), entries in buckets.items():
+                tl = B.TensorList(entries)
+                need = B.layerwise_workspace_bytes(tl)
+                if self._workspace is None or self._workspace.numel() < need:
+                    self._workspace = torch.empty(need, dtype=torch.uint8, device=tl.device)
+                scales = B.optim8bit_step_layerwise(self.kind, tl, lr=group["lr"], step=step, hp=hp,
+                                                    trust_coefficient=eta, workspace=self._workspace).clone()
+                for i, e in enumerate(entries):
+                    self.state[e[0]]["trust_scale"] = scales[i]
+        return loss
+
+
+class LAMB8bit(_LayerwiseOptimizer8bit):
+    """LAMB (You et al. 2020, Alg. 2; T5 P:366) with 8-bit block-wise dynamic states: Adam
+    moments, u = m_hat/(sqrt(r_hat)+eps) + wd*w, w -= lr * ||w||/||u|| * u per tensor."""
+    kind = "lamb"
+
+    def __init__(self, params, lr=1e-3, betas=(0.9, 0.999), eps=1e-6, weight_decay=0.01, bias_correction=True):
+        super().__init__(params, lr, betas, eps, weight_decay, bias_correction)
+
+
+class LARS8bit(_LayerwiseOptimizer8bit):
+    """LARS (You et al. 2017, Alg. 1; T5 P:367) with an 8-bit block-wise momentum state:
+    v = momentum*v + lr * eta*||w||/(||g|| + wd*||w||) * (g + wd*w), w -= v per tensor."""
+    kind = "lars"
+
+    def __init__(self, params, lr=0.1, momentum=0.9, weight_decay=5e-4, trust_coefficient=0.001):
+        if trust_coefficient <= 0:
+            raise ValueError("trust_coefficient must be > 0")
+        super().__init__(params, lr, (momentum, 0.0), 1e-8, weight_decay, False)
+        for group in self.param_groups:
+            group.setdefault("trust_coefficient", trust_coefficient)
+
+
 def state_bytes(n_params: int, kind: str = "adam", blocksize: int = B.BLOCKSIZE) -> int:
     """Optimizer-state bytes of the 8-bit optimizer: 1 B per element per state plus one fp32
     absmax per block per state (8 GB -> 2 GB for a 1B-parameter Adam)."""
-    states = 1 if kind == "momentum" else 2
+    states = 2 if kind in _TWO_STATES else 1
     return states * (n_params + 4 * B.nblocks(n_params, blocksize))

@@ -105,3 +105,32 @@ def test_host_linear_codebook_matches_oracle(signed):
     a = q8.create_linear_codebook(signed).numpy()
     b = oracle.linear_codebook(signed)
     assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def _lw(kind=B.Q8_LAMB, trust=0.001, ws=FAKE, ws_bytes=1 << 20, arr=None, count=1, hp=None):
+    if arr is None:
+        arr = (B.TensorDesc * 1)()
+        arr[0] = B.TensorDesc(FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 5000)
+    return B.lib.q8_optim8bit_step_layerwise(kind, B.Q8_BF16, arr, count, 2048, ctypes.byref(hp or _hp(eps=1e-6)),
+                                             trust, 1, ws, ws_bytes, None)
+
+
+def test_layerwise_workspace_bytes():
+    arr = (B.TensorDesc * 3)()
+    for i, n in enumerate((5000, 0, 2048)):
+        arr[i] = B.TensorDesc(FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, n)
+    # scales: 3 floats -> 16 B; partials: (3 + 0 + 1) blocks x 16 B
+    assert B.lib.q8_layerwise_workspace_bytes(arr, 3) == 16 + 4 * 16
+    assert B.lib.q8_layerwise_workspace_bytes(arr, -1) == -1
+
+
+def test_layerwise_validation():
+    assert _lw(kind=B.Q8_ADAM) == B.Q8_ERR_INVALID
+    assert _lw(kind=B.Q8_LARS, trust=0.0) == B.Q8_ERR_INVALID
+    assert _lw(ws_bytes=16) == B.Q8_ERR_INVALID and "workspace too small" in B.lib.q8_last_error().decode()
+    assert _lw(ws=FAKE + 8) == B.Q8_ERR_INVALID
+    assert _lw(hp=_hp(eps=0.0)) == B.Q8_ERR_INVALID
+    # layer-wise kinds are rejected by the element-wise entry points
+    rc = B.lib.q8_optim8bit_step(B.Q8_LAMB, FAKE, FAKE, B.Q8_BF16, FAKE, FAKE, FAKE, FAKE, 4096, 2048,
+                                 ctypes.byref(_hp()), 1, None)
+    assert rc == B.Q8_ERR_INVALID and "layer-wise" in B.lib.q8_last_error().decode()

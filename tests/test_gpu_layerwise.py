@@ -1,0 +1,147 @@
+"""GPU parity of the layer-wise 8-bit optimizers (8-bit LAMB / LARS, T5 P:366-367; readings L1-L4)
+through the C ABI (q8_optim8bit_step_layerwise) against the oracle, tensor by tensor.
+
+Every output is compared bit for bit: the per-tensor scales RN(lr * ratio), the parameters, the
+codes and the absmax values.  The norms are binary64 sums in different orders on the two sides
+(L3), so the scales could in principle differ in their last bit; with the seeded inputs below
+they are identical, and given identical scales every other output is a unique function of the
+inputs (as for the element-wise step)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+LAMB = dict(synth.HPARAMS["lamb"])
+LARS = dict(synth.HPARAMS["lars"])
+ETA = LARS.pop("trust_coefficient")
+HP = {"lamb": LAMB, "lars": LARS}
+
+
+@pytest.fixture(scope="module")
+def q8():
+    import paper_2110_02861_b200 as m
+    return m
+
+
+def _make(kind, sizes, gdt, seed0=0):
+    two = kind == "lamb"
+    ents, refs = [], []
+    for i, n in enumerate(sizes):
+        p = synth.params(n, seed=seed0 + i)
+        s1, a1 = synth.random_state(n, seed=seed0 + 100 + i, scale=1e-3)
+        s2, a2 = synth.random_state(n, seed=seed0 + 200 + i, scale=1e-6)
+        ents.append([p.to(DEV), None, s1.to(DEV), s2.to(DEV) if two else None, a1.to(DEV), a2.to(DEV) if two else None])
+        refs.append([p.numpy().copy(), s1.numpy().copy(), s2.numpy().copy(), a1.numpy().copy(), a2.numpy().copy()])
+    return ents, refs
+
+
+def _step_both(q8, kind, ents, refs, sizes, gdt, t, hp):
+    gs = [synth.grads(n, step=t, seed=7 + i, dtype=gdt) for i, n in enumerate(sizes)]
+    for e, g in zip(ents, gs):
+        e[1] = g.to(DEV)
+    scales = q8.optim8bit_step_layerwise(kind, [tuple(e) for e in ents], step=t, trust_coefficient=ETA, **hp)
+    torch.cuda.synchronize()
+    exp = []
+    for r, g in zip(refs, gs):
+        two = kind == "lamb"
+        exp.append(oracle.optim8bit_layerwise_step(kind, r[0], synth.to_f32_numpy(g), r[1], r[2] if two else None,
+                                                   r[3], r[4] if two else None, step=t, trust_coefficient=ETA, **hp))
+    return scales.cpu().numpy(), np.array(exp, np.float32)
+
+
+def _assert_equal(kind, ents, refs):
+    for i, (e, r) in enumerate(zip(ents, refs)):
+        assert np.array_equal(e[0].cpu().numpy().view(np.uint32), r[0].view(np.uint32)), f"p of tensor {i}"
+        assert np.array_equal(e[2].cpu().numpy(), r[1]), f"s1 of tensor {i}"
+        assert np.array_equal(e[4].cpu().numpy().view(np.uint32), r[3].view(np.uint32)), f"absmax1 of tensor {i}"
+        if kind == "lamb":
+            assert np.array_equal(e[3].cpu().numpy(), r[2]), f"s2 of tensor {i}"
+            assert np.array_equal(e[5].cpu().numpy().view(np.uint32), r[4].view(np.uint32)), f"absmax2 of tensor {i}"
+
+
+@pytest.mark.parametrize("kind", ["lamb", "lars"])
+@pytest.mark.parametrize("gdt", ["float32", "float16", "bfloat16"])
+def test_layerwise_matches_oracle(q8, kind, gdt):
+    sizes = [1, 17, 2047, 2049, 3 * 2048 + 5, 100_003, 1 << 20]
+    ents, refs = _make(kind, sizes, gdt)
+    for t in (1, 2, 3):
+        got, exp = _step_both(q8, kind, ents, refs, sizes, gdt, t, HP[kind])
+        assert np.array_equal(got.view(np.uint32), exp.view(np.uint32)), (t, got, exp)
+    _assert_equal(kind, ents, refs)
+
+
+@pytest.mark.parametrize("kind", ["lamb", "lars"])
+def test_layerwise_hparam_variants(q8, kind):
+    sizes = [5000, 70_001]
+    variants = ([dict(LAMB, weight_decay=0.0), dict(LAMB, bias_correction=False), dict(LAMB, lr=0.02, beta2=0.99)]
+                if kind == "lamb" else [dict(LARS, weight_decay=0.0), dict(LARS, beta1=0.0), dict(LARS, lr=1.0)])
+    for j, hp in enumerate(variants):
+        ents, refs = _make(kind, sizes, "bfloat16", seed0=10 * j)
+        for t in (1, 4):
+            got, exp = _step_both(q8, kind, ents, refs, sizes, "bfloat16", t, hp)
+            assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
+        _assert_equal(kind, ents, refs)
+
+
+@pytest.mark.parametrize("kind", ["lamb", "lars"])
+def test_layerwise_zero_tensors_and_empty(q8, kind):
+    """A zero weight tensor (trust ratio falls back to 1, L1/L2) and empty tensors (scale = lr)."""
+    sizes = [4096, 0, 3000, 0]
+    ents, refs = _make(kind, sizes, "float32")
+    ents[0][0].zero_()
+    refs[0][0][:] = 0
+    got, exp = _step_both(q8, kind, ents, refs, sizes, "float32", 1, HP[kind])
+    assert got[1] == np.float32(HP[kind]["lr"]) and got[3] == np.float32(HP[kind]["lr"])
+    assert got[0] == exp[0] and got[2] == exp[2]
+    _assert_equal(kind, ents, refs)
+
+
+def test_layerwise_chunks_over_384_tensors(q8):
+    """More tensors than one launch takes: the workspace's partials are reused per chunk."""
+    rng = np.random.default_rng(5)
+    sizes = [int(x) for x in rng.integers(1, 9000, size=400)]
+    ents, refs = _make("lars", sizes, "bfloat16")
+    got, exp = _step_both(q8, "lars", ents, refs, sizes, "bfloat16", 1, LARS)
+    assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
+    _assert_equal("lars", ents, refs)
+
+
+def test_lars_resnet50_layer_list(q8):
+    """LARS's home workload: the 161 ResNet-50 tensors, bf16 grads, 2 steps."""
+    sizes = [int(np.prod(s)) for s in synth.resnet50_shapes()]
+    ents, refs = _make("lars", sizes, "bfloat16")
+    for t in (1, 2):
+        got, exp = _step_both(q8, "lars", ents, refs, sizes, "bfloat16", t, LARS)
+        assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
+    _assert_equal("lars", ents, refs)
+
+
+@pytest.mark.parametrize("cls,kind", [("LAMB8bit", "lamb"), ("LARS8bit", "lars")])
+def test_layerwise_optimizer_api(q8, cls, kind):
+    torch.manual_seed(0)
+    model = torch.nn.Sequential(torch.nn.Linear(300, 700), torch.nn.LayerNorm(700), torch.nn.Linear(700, 50)).to(DEV)
+    ref = [p.detach().cpu().numpy().copy().reshape(-1) for p in model.parameters()]
+    if kind == "lamb":
+        opt = q8.LAMB8bit(model.parameters(), lr=2e-3, weight_decay=0.01)
+        hp = dict(lr=2e-3, beta1=0.9, beta2=0.999, eps=1e-6, weight_decay=0.01, bias_correction=True)
+    else:
+        opt = q8.LARS8bit(model.parameters(), lr=0.1, momentum=0.9, weight_decay=5e-4, trust_coefficient=0.001)
+        hp = dict(lr=0.1, beta1=0.9, beta2=0.0, eps=1e-8, weight_decay=5e-4, bias_correction=False)
+    st = [[np.zeros(r.size, np.uint8), np.zeros(r.size, np.uint8), np.zeros((r.size + 2047) // 2048, np.float32),
+           np.zeros((r.size + 2047) // 2048, np.float32)] for r in ref]
+    x = torch.randn(64, 300, device=DEV)
+    for t in (1, 2, 3):
+        opt.zero_grad()
+        model(x).square().mean().backward()
+        grads = [p.grad.detach().cpu().numpy().copy().reshape(-1) for p in model.parameters()]
+        opt.step()
+        for r, g, s in zip(ref, grads, st):
+            oracle.optim8bit_layerwise_step(kind, r, g, s[0], s[1] if kind == "lamb" else None, s[2],
+                                            s[3] if kind == "lamb" else None, step=t, trust_coefficient=0.001, **hp)
+    for p, r in zip(model.parameters(), ref):
+        assert np.array_equal(p.detach().cpu().numpy().reshape(-1).view(np.uint32), r.view(np.uint32))
+        assert "trust_scale" in opt.state[p]
