@@ -594,6 +594,7 @@ q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_t
         P.block_start[k] = blocks;
         P.total_blocks = blocks;
         P.scale = scale + c;
+        P.partial = partial;
         cudaError_t e = cudaErrorInvalidValue;
         switch (g_dtype) {
             case Q8_F32: e = q8::launch_layerwise_g0(kind, P, ctx, partial, scale + c, hp->lr, trust_coefficient,

@@ -77,6 +77,7 @@ template <int MAXT>
 struct StepParams {
     StepScalars s;
     const float* scale;             // LAMB / LARS: per-tensor trust scale RN(lr*ratio) (L1-L3)
+    double2* partial;               // LAMB norms pass: per-block (sum w^2, sum u^2)
     int num_tensors;
     int64_t total_blocks;
     int64_t block_start[MAXT + 1];  // prefix sums of per-tensor block counts
@@ -210,12 +211,17 @@ __device__ __forceinline__ void update_element(const StepScalars& s, float& w, f
 
 // ---------------------------------------------------------------------------- step kernel
 
+// Tensor of global block b: the largest t with block_start[t] <= b.  `from` is a tensor known to
+// start at or before b (grid-stride loops visit blocks in increasing order, so the previous
+// answer is one): the common case -- b still inside tensor `from` -- costs one compare instead of
+// a dependent binary search over the launch's parameter-space table.
 template <int MAXT>
-__device__ __forceinline__ int find_tensor(const StepParams<MAXT>& P, int64_t b) {
+__device__ __forceinline__ int find_tensor(const StepParams<MAXT>& P, int64_t b, int from = 0) {
     if constexpr (MAXT == 1) {
         return 0;
     } else {
-        int lo = 0, hi = P.num_tensors - 1;  // largest t with block_start[t] <= b
+        if (from + 1 >= P.num_tensors || P.block_start[from + 1] > b) return from;
+        int lo = from + 1, hi = P.num_tensors - 1;
         while (lo < hi) {
             int mid = (lo + hi + 1) >> 1;
             if (P.block_start[mid] <= b) lo = mid; else hi = mid - 1;

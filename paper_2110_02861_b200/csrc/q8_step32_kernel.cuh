@@ -14,8 +14,9 @@ __global__ void __launch_bounds__(kThreads) optim32bit_step_kernel(const __grid_
     constexpr bool kTwo = (KIND != KIND_MOMENTUM);
     const StepScalars S = P.s;
     const int tid = threadIdx.x;
+    int ti = 0;
     for (int64_t gb = blockIdx.x; gb < P.total_blocks; gb += gridDim.x) {
-        const int ti = find_tensor<MAXT>(P, gb);
+        ti = find_tensor<MAXT>(P, gb, ti);
         const TensorDesc& T = P.t[ti];
         const int64_t base = (gb - P.block_start[ti]) * kBlock;
         float* __restrict__ m = reinterpret_cast<float*>(T.s1) + base;

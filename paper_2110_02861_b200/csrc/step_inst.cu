@@ -69,22 +69,28 @@ cudaError_t launch_layerwise_t(const StepParams<kMultiMaxT>& P, const LaunchCtx&
     constexpr int G = Q8_GDT;
     constexpr int NS = G == G_F32 ? 3 : 4;
     constexpr int SUBT = G == G_F32 ? 256 : 128;
-    static int occ = [] {
-        int o = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, layer_norms_kernel<KIND, G, kMultiMaxT>, kThreads, 0) !=
-                cudaSuccess || o < 1)
-            o = 1;
-        return o;
-    }();
     if (P.total_blocks == 0) {  // only empty tensors: their scale is still defined (lr)
-        layer_scale_kernel<KIND, kMultiMaxT><<<P.num_tensors, 32, 0, ctx.stream>>>(P, partial, scale, lr, eta, wd);
+        layer_scale_kernel<KIND, kMultiMaxT><<<P.num_tensors, kThreads, 0, ctx.stream>>>(P, partial, scale, lr, eta, wd);
         return cudaGetLastError();
     }
-    const int64_t g1 = std::min<int64_t>(P.total_blocks, static_cast<int64_t>(ctx.sms) * occ);
-    layer_norms_kernel<KIND, G, kMultiMaxT><<<static_cast<unsigned>(g1), kThreads, 0, ctx.stream>>>(P, ctx.tabs, partial);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e;
+    if constexpr (KIND == KIND_LAMB) {
+        e = persistent(optim8bit_step_kernel<KIND, G, kMultiMaxT, SEARCH_BUCKET, NS, SUBT, MODE_NORMS>, NS, SUBT,
+                       P.total_blocks, ctx, P, ctx.tabs);
+    } else {
+        static int occ = [] {
+            int o = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, lars_norms_kernel<G, kMultiMaxT>, kThreads, 0) !=
+                    cudaSuccess || o < 1)
+                o = 1;
+            return o;
+        }();
+        const int64_t g1 = std::min<int64_t>(P.total_blocks, static_cast<int64_t>(ctx.sms) * occ);
+        lars_norms_kernel<G, kMultiMaxT><<<static_cast<unsigned>(g1), kThreads, 0, ctx.stream>>>(P);
+        e = cudaGetLastError();
+    }
     if (e != cudaSuccess) return e;
-    layer_scale_kernel<KIND, kMultiMaxT><<<P.num_tensors, 32, 0, ctx.stream>>>(P, partial, scale, lr, eta, wd);
+    layer_scale_kernel<KIND, kMultiMaxT><<<P.num_tensors, kThreads, 0, ctx.stream>>>(P, partial, scale, lr, eta, wd);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     return persistent(optim8bit_step_kernel<KIND, G, kMultiMaxT, SEARCH_BUCKET, NS, SUBT>, NS, SUBT, P.total_blocks,

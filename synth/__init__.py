@@ -79,6 +79,12 @@ WORKLOADS = {
                          desc="8-bit AdamW, 1.5B GPT-2-XL flat buffer, bf16 grads"),
     "cfg5_t5_11b": dict(kind="adam", grad_dtype="bfloat16", shapes=t5_11b_shapes(),
                         desc="8-bit Adam, 11B T5-shaped flat buffer, ZeRO-1 over 8 GPUs"),
+    # SURVEY 8(f) row 3 (T5 P:366-367): layer-wise optimizers over real layer lists (one trust
+    # ratio per tensor), measured with the same bench contract
+    "lamb_gpt2_xl": dict(kind="lamb", grad_dtype="bfloat16", shapes=gpt2_shapes(1600, 48), layerwise=True,
+                         desc="8-bit LAMB, GPT-2-XL 580-tensor layer list, bf16 grads"),
+    "lars_resnet50": dict(kind="lars", grad_dtype="float16", shapes=resnet50_shapes(), layerwise=True,
+                          desc="8-bit LARS, ResNet-50 161-tensor layer list, fp16 grads"),
 }
 
 HPARAMS = {
