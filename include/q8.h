@@ -205,6 +205,39 @@ q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_t
  * tensor (rounded up to 16) + 16 per 2048-block of the largest launch chunk.  -1 on bad input. */
 int64_t q8_layerwise_workspace_bytes(const q8_tensor* tensors_host, int32_t num_tensors);
 
+/* Fused ZeRO-1 step over peer memory: ONE kernel per rank does
+ * the reduce-scatter of the gradients, the fused 8-bit step of this rank's shard and the
+ * all-gather of the updated parameters, reading and writing the other ranks' buffers directly
+ * (NVLink peer access / CUDA IPC mappings), tile by tile, so the transfers overlap the step.
+ * The flat buffers of n_pad elements (a multiple of world*2048) are split into world shards of
+ * n_pad/world on block boundaries (blocks are independent, so sharding is exact).
+ *   g_peers_host[r]   rank r's full gradient buffer (n_pad elements of g_dtype), readable here
+ *   p_peers_host[r]   rank r's full fp32 parameter buffer (n_pad), writable here; this rank's own
+ *                     shard is read from p_peers_host[rank]
+ *   sig_peers_host[r] rank r's signal pad, q8_zero_signal_bytes(world, num_ctas) bytes, zeroed once
+ *                     at allocation and then owned by these calls
+ *   s1, s2, absmax1, absmax2  this rank's shard states (n_pad/world codes, n_pad/world/2048 absmax)
+ * (the three peer arrays are HOST arrays of device pointers, copied into the launch)
+ * Reading Z1: g = (g_0 + ... + g_{world-1}) / world per element -- binary32 adds in rank order,
+ * IEEE division; then the step of q8_optim8bit_step on the shard, and every rank's buffer receives
+ * the shard's new parameters.  Synchronisation: CTA i of every rank raises its flag (= epoch) in
+ * every rank's pad and waits for all ranks' flags before reading gradients, and again after its
+ * parameter writes; so when the call completes on `stream`, every rank's gradients have been
+ * consumed and this rank's parameter buffer holds all shards.  epoch must start at 1 and grow by
+ * one per call (the pads are never reset); every rank must make the same sequence of calls with
+ * the same num_ctas (0 = one CTA per SM; all ranks' CTAs must be co-resident: on a shared GPU use
+ * num_ctas <= SMs / world).  A rank that never arrives makes the kernel trap after ~30 s.
+ * world <= 16.  Errors: as q8_optim8bit_step, plus INVALID for bad world/rank/n_pad/epoch/num_ctas. */
+q8_status q8_optim8bit_step_zero_fused(q8_kind kind, q8_dtype g_dtype, int32_t world, int32_t rank,
+                                       const void* const* g_peers_host, float* const* p_peers_host,
+                                       uint32_t* const* sig_peers_host, uint8_t* s1, uint8_t* s2, float* absmax1,
+                                       float* absmax2, int64_t n_pad, int32_t blocksize, const q8_hparams* hp,
+                                       int64_t step, uint32_t epoch, int32_t num_ctas, void* stream);
+
+/* Bytes of one rank's signal pad for q8_optim8bit_step_zero_fused: 2 * world * num_ctas * 4
+ * (num_ctas 0 = the current device's SM count).  -1 on bad input. */
+int64_t q8_zero_signal_bytes(int32_t world, int32_t num_ctas);
+
 /* Thread-local description of the last error ("" after success). */
 const char* q8_last_error(void);
 

@@ -25,7 +25,8 @@ EXPORTS = ("q8_create_dynamic_codebook", "q8_create_linear_codebook", "q8_quanti
            "q8_quantize_blockwise_dynamic", "q8_dequantize_blockwise", "q8_quantize_tensorwise",
            "q8_dequantize_tensorwise",
            "q8_optim8bit_step", "q8_optim8bit_step_multi", "q8_optim32bit_step_multi",
-           "q8_optim8bit_step_layerwise", "q8_layerwise_workspace_bytes", "q8_last_error", "q8_version")
+           "q8_optim8bit_step_layerwise", "q8_layerwise_workspace_bytes", "q8_optim8bit_step_zero_fused",
+           "q8_zero_signal_bytes", "q8_last_error", "q8_version")
 
 
 class Q8Error(RuntimeError):
@@ -69,9 +70,14 @@ def _load():
     lib.q8_optim8bit_step_layerwise.argtypes = [i32, i32, ctypes.POINTER(TensorDesc), i32, i32,
                                                 ctypes.POINTER(HParams), ctypes.c_double, i64, vp, i64, vp]
     lib.q8_layerwise_workspace_bytes.argtypes = [ctypes.POINTER(TensorDesc), i32]
+    lib.q8_optim8bit_step_zero_fused.argtypes = [i32, i32, i32, i32, ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                                 ctypes.POINTER(vp), vp, vp, vp, vp, i64, i32, ctypes.POINTER(HParams),
+                                                 i64, ctypes.c_uint32, i32, vp]
+    lib.q8_zero_signal_bytes.argtypes = [i32, i32]
     for f in EXPORTS[:-2]:
         getattr(lib, f).restype = ctypes.c_int
     lib.q8_layerwise_workspace_bytes.restype = i64
+    lib.q8_zero_signal_bytes.restype = i64
     lib.q8_last_error.restype = ctypes.c_char_p
     lib.q8_version.restype = ctypes.c_char_p
     return lib
@@ -312,3 +318,25 @@ def optim8bit_step_layerwise(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1
                                                                                          "workspace"),
                                            workspace.numel(), _stream(tl.device)))
     return workspace[:4 * tl.count].view(torch.float32)
+
+
+def zero_signal_bytes(world: int, num_ctas: int = 0) -> int:
+    nb = lib.q8_zero_signal_bytes(int(world), int(num_ctas))
+    if nb < 0:
+        raise ValueError("invalid world / num_ctas")
+    return nb
+
+
+def optim8bit_step_zero_fused(kind, world, rank, g_ptrs, p_ptrs, sig_ptrs, s1, s2, absmax1, absmax2, n_pad, g_dtype,
+                              *, step, epoch, num_ctas=0, stream=None, hp: HParams):
+    """Fused ZeRO-1 step over peer memory (q8_optim8bit_step_zero_fused): g_ptrs / p_ptrs /
+    sig_ptrs are per-rank device addresses (ints) of the gradient, parameter and signal buffers."""
+    kind = KINDS.get(kind, kind)
+    arr = ctypes.c_void_p * world
+    _check(lib.q8_optim8bit_step_zero_fused(kind, GDTYPES[g_dtype], world, rank, arr(*g_ptrs), arr(*p_ptrs),
+                                            arr(*sig_ptrs), _dev_ptr(s1, torch.uint8, "s1"),
+                                            _dev_ptr(s2, torch.uint8, "s2"),
+                                            _dev_ptr(absmax1, torch.float32, "absmax1"),
+                                            _dev_ptr(absmax2, torch.float32, "absmax2"), int(n_pad), BLOCKSIZE,
+                                            ctypes.byref(hp), int(step), int(epoch), int(num_ctas),
+                                            stream if stream is not None else _stream(s1.device)))

@@ -610,3 +610,81 @@ q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_t
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- fused ZeRO-1 step + peer memory
+
+extern "C" {
+
+int64_t q8_zero_signal_bytes(int32_t world, int32_t num_ctas) {
+    if (world < 1 || world > q8::kMaxWorld || num_ctas < 0) return -1;
+    int ctas = num_ctas;
+    if (ctas == 0) {
+        DeviceState* d = nullptr;
+        if (device_state(&d) != Q8_OK) return -1;
+        ctas = d->sms;
+    }
+    return static_cast<int64_t>(2) * world * ctas * 4;
+}
+
+q8_status q8_optim8bit_step_zero_fused(q8_kind kind, q8_dtype g_dtype, int32_t world, int32_t rank,
+                                       const void* const* g_peers_host, float* const* p_peers_host,
+                                       uint32_t* const* sig_peers_host, uint8_t* s1, uint8_t* s2, float* absmax1,
+                                       float* absmax2, int64_t n_pad, int32_t blocksize, const q8_hparams* hp,
+                                       int64_t step, uint32_t epoch, int32_t num_ctas, void* stream) {
+    if (q8_status s = reject_layerwise(kind); s != Q8_OK) return s;
+    if (q8_status s = check_common(g_dtype, blocksize); s != Q8_OK) return s;
+    if (q8_status s = validate_hparams(kind, hp, step); s != Q8_OK) return s;
+    if (world < 1 || world > q8::kMaxWorld) return fail(Q8_ERR_INVALID, "world must be in [1, %d]", q8::kMaxWorld);
+    if (rank < 0 || rank >= world) return fail(Q8_ERR_INVALID, "rank %d out of [0, %d)", rank, world);
+    if (n_pad < 0 || n_pad % (static_cast<int64_t>(world) * q8::kBlock) != 0)
+        return fail(Q8_ERR_INVALID, "n_pad must be a multiple of world * 2048 (ZeRO padding)");
+    if (epoch == 0) return fail(Q8_ERR_INVALID, "epoch must be >= 1 (signal pads start zeroed)");
+    if (n_pad == 0) return ok();
+    if (!g_peers_host || !p_peers_host || !sig_peers_host) return fail(Q8_ERR_INVALID, "peer arrays are NULL");
+    for (int r = 0; r < world; ++r) {
+        if (!g_peers_host[r] || !p_peers_host[r] || !sig_peers_host[r])
+            return fail(Q8_ERR_INVALID, "rank %d: NULL peer pointer", r);
+        if (!aligned(g_peers_host[r], 16) || !aligned(p_peers_host[r], 16) || !aligned(sig_peers_host[r], 4))
+            return fail(Q8_ERR_INVALID, "rank %d: peer buffers must be 16-byte aligned", r);
+    }
+    const int64_t shard = n_pad / world;
+    q8_tensor t{p_peers_host[rank] + static_cast<int64_t>(rank) * shard, g_peers_host[rank], s1, s2, absmax1, absmax2,
+                shard};
+    if (q8_status s = validate_tensor(kind, g_dtype, t, 0); s != Q8_OK) return s;
+    DeviceState* d = nullptr;
+    if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    const int grid = num_ctas == 0 ? d->sms : num_ctas;
+    if (grid < 1 || grid > d->sms)
+        return fail(Q8_ERR_INVALID, "num_ctas must be in [1, %d] (all CTAs of all ranks must be co-resident)", d->sms);
+    q8::StepParams<1> P;
+    P.s = make_scalars(hp, step);
+    P.scale = nullptr;
+    P.partial = nullptr;
+    P.num_tensors = 1;
+    P.block_start[0] = 0;
+    P.total_blocks = P.block_start[1] = shard / q8::kBlock;
+    P.t[0] = q8::TensorDesc{t.p, nullptr, s1, s2, absmax1, absmax2, shard};
+    std::memset(&P.z, 0, sizeof P.z);
+    for (int r = 0; r < world; ++r) {
+        P.z.g[r] = g_peers_host[r];
+        P.z.p[r] = p_peers_host[r];
+        P.z.sig[r] = sig_peers_host[r];
+    }
+    P.z.off = static_cast<int64_t>(rank) * shard;
+    P.z.world = world;
+    P.z.rank = rank;
+    P.z.epoch = epoch;
+    P.z.pow2 = (world & (world - 1)) == 0;
+    P.z.invw = static_cast<float>(1.0 / world);
+    const q8::LaunchCtx ctx{d->tabs, d->sms, static_cast<cudaStream_t>(stream), q8::SEARCH_BUCKET, 0, 0};
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (g_dtype) {
+        case Q8_F32: e = q8::launch_zero_g0(kind, P, ctx, grid); break;
+        case Q8_F16: e = q8::launch_zero_g1(kind, P, ctx, grid); break;
+        case Q8_BF16: e = q8::launch_zero_g2(kind, P, ctx, grid); break;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "fused ZeRO step launch");
+    return ok();
+}
+
+}  // extern "C"

@@ -73,11 +73,29 @@ struct StepScalars {       // all computed on the host in double, rounded once (
     int fast_div;          // eps_hat >= 2^-40: the packed sqrt/div fast path may be used
 };
 
+// Fused ZeRO-1 step over peer memory: every rank's full padded
+// gradient and parameter buffers and its signal pad, mapped into this GPU's address space
+// (NVLink P2P / CUDA IPC).  Reading Z1: the shard gradient is the rank-order binary32 sum of the
+// ranks' gradients divided by world (IEEE; a multiply by the exact reciprocal when world is a
+// power of two); the updated shard parameters are written into every rank's buffer.
+constexpr int kMaxWorld = 16;
+struct ZeroParams {
+    const void* g[kMaxWorld];
+    float* p[kMaxWorld];
+    uint32_t* sig[kMaxWorld];   // [2 phases][world][grid] uint32 flags (epochs)
+    int64_t off;                // first element of this rank's shard
+    int world, rank;
+    uint32_t epoch;             // this call's flag value (strictly increasing, >= 1)
+    float invw;                 // 1/world (exact when pow2)
+    int pow2;
+};
+
 template <int MAXT>
 struct StepParams {
     StepScalars s;
     const float* scale;             // LAMB / LARS: per-tensor trust scale RN(lr*ratio) (L1-L3)
     double2* partial;               // LAMB norms pass: per-block (sum w^2, sum u^2)
+    ZeroParams z;                   // fused ZeRO-1 mode only
     int num_tensors;
     int64_t total_blocks;
     int64_t block_start[MAXT + 1];  // prefix sums of per-tensor block counts

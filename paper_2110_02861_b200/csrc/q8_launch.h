@@ -37,6 +37,12 @@ cudaError_t launch_layerwise_g1(int kind, const StepParams<kMultiMaxT>& P, const
 cudaError_t launch_layerwise_g2(int kind, const StepParams<kMultiMaxT>& P, const LaunchCtx& ctx, double2* partial,
                                 float* scale, double lr, double eta, double wd);
 
+// Fused ZeRO-1 step (MODE_ZERO) for gradient dtype g<N> with exactly `grid` CTAs (identical on
+// every rank: the cross-rank barrier pairs CTA i with CTA i).
+cudaError_t launch_zero_g0(int kind, const StepParams<1>& P, const LaunchCtx& ctx, int grid);
+cudaError_t launch_zero_g1(int kind, const StepParams<1>& P, const LaunchCtx& ctx, int grid);
+cudaError_t launch_zero_g2(int kind, const StepParams<1>& P, const LaunchCtx& ctx, int grid);
+
 // Opt a kernel into `smem` bytes of dynamic shared memory (once per kernel and thread).
 cudaError_t ensure_smem(const void* fn, int smem);
 

@@ -116,3 +116,29 @@ cudaError_t Q8_CAT(launch_layerwise_g, Q8_GDT)(int kind, const StepParams<kMulti
     return cudaErrorInvalidValue;
 }
 }  // namespace q8
+
+namespace q8 {
+namespace {
+template <int KIND>
+cudaError_t launch_zero_t(const StepParams<1>& P, const LaunchCtx& ctx, int grid) {
+    constexpr int G = Q8_GDT;
+    constexpr int NS = G == G_F32 ? 3 : 4;
+    constexpr int SUBT = G == G_F32 ? 256 : 128;
+    const auto fn = optim8bit_step_kernel<KIND, G, 1, SEARCH_BUCKET, NS, SUBT, MODE_ZERO>;
+    const int smem = step_smem_bytes(NS, G);
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
+    if (e != cudaSuccess) return e;
+    fn<<<static_cast<unsigned>(grid), NS * SUBT, smem, ctx.stream>>>(P, ctx.tabs);
+    return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t Q8_CAT(launch_zero_g, Q8_GDT)(int kind, const StepParams<1>& P, const LaunchCtx& ctx, int grid) {
+    switch (kind) {
+        case KIND_ADAM: return launch_zero_t<KIND_ADAM>(P, ctx, grid);
+        case KIND_ADAMW: return launch_zero_t<KIND_ADAMW>(P, ctx, grid);
+        case KIND_MOMENTUM: return launch_zero_t<KIND_MOMENTUM>(P, ctx, grid);
+        default: return cudaErrorInvalidValue;
+    }
+}
+}  // namespace q8

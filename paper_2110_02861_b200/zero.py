@@ -88,3 +88,82 @@ class Zero1Optimizer8bit:
         self.reduce_scatter()
         self.shard_step()
         self.all_gather()
+
+
+def exchange_peer_tensors(tensors, group=None):
+    """Map every rank's `tensors` into this process (CUDA IPC through torch's tensor sharing, the
+    handles travelling over the process group).  Returns peers[r][k] = rank r's k-th tensor as a
+    tensor of this process (own rank: the tensor itself).  Works across GPUs of a node (NVLink peer
+    mappings) and between processes sharing one GPU."""
+    from torch.multiprocessing.reductions import reduce_tensor
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    mine = [reduce_tensor(t) for t in tensors]
+    allh = [None] * world
+    dist.all_gather_object(allh, mine, group=group)
+    peers = []
+    for r in range(world):
+        if r == rank:
+            peers.append(list(tensors))
+        else:
+            peers.append([fn(*args) for fn, args in allh[r]])
+    return peers
+
+
+class ZeroFusedOptimizer8bit:
+    """ZeRO-1 with the reduce-scatter, the 8-bit shard step and the all-gather fused into ONE kernel
+    per rank over peer memory (q8_optim8bit_step_zero_fused): each rank reads
+    its shard's gradients from every rank's buffer, steps the shard and writes the new values into
+    every rank's parameter buffer, tile by tile; CTAs of the ranks meet at flag barriers in each
+    rank's signal pad.  Buffers as Zero1Optimizer8bit (flat, padded to world*2048); the gradient
+    of a shard is the rank-order binary32 sum / world (reading Z1).
+
+    num_ctas: CTAs per rank (0 = one per SM).  Ranks that share one GPU (tests) must use at most
+    SMs / world each so that every CTA of every rank can be resident."""
+
+    def __init__(self, n_params: int, kind: str = "adamw", grad_dtype=torch.bfloat16, device=None, group=None,
+                 num_ctas: int = 0, **hparams):
+        if kind not in ("adam", "adamw", "momentum"):
+            raise ValueError("the fused ZeRO step takes adam / adamw / momentum")
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.kind = kind
+        self.n = n_params
+        self.n_pad = padded_numel(n_params, self.world)
+        self.lo, self.hi = shard_range(self.n_pad, self.world, self.rank)
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.num_ctas = num_ctas
+        self.params = torch.zeros(self.n_pad, dtype=torch.float32, device=dev)
+        self.grads = torch.zeros(self.n_pad, dtype=grad_dtype, device=dev)
+        self.signal = torch.zeros(B.zero_signal_bytes(self.world, num_ctas), dtype=torch.uint8, device=dev)
+        shard = self.hi - self.lo
+        two = kind != "momentum"
+        self.s1 = torch.zeros(shard, dtype=torch.uint8, device=dev)
+        self.absmax1 = torch.zeros(shard // B.BLOCKSIZE, dtype=torch.float32, device=dev)
+        self.s2 = torch.zeros(shard, dtype=torch.uint8, device=dev) if two else None
+        self.absmax2 = torch.zeros(shard // B.BLOCKSIZE, dtype=torch.float32, device=dev) if two else None
+        self.hp = B.hparams(**hparams)
+        self.t = 0
+        self.epoch = 0
+        torch.cuda.synchronize(dev)
+        if self.world > 1:
+            self._peers = exchange_peer_tensors([self.grads, self.params, self.signal], group)
+            dist.barrier(group)
+        else:
+            self._peers = [[self.grads, self.params, self.signal]]
+        self._g = [pt[0].data_ptr() for pt in self._peers]
+        self._p = [pt[1].data_ptr() for pt in self._peers]
+        self._sig = [pt[2].data_ptr() for pt in self._peers]
+
+    @property
+    def p_shard(self) -> torch.Tensor:
+        return self.params[self.lo:self.hi]
+
+    def step(self):
+        """One fused reduce-scatter + 8-bit step + all-gather (a single kernel launch)."""
+        self.t += 1
+        self.epoch += 1
+        B.optim8bit_step_zero_fused(self.kind, self.world, self.rank, self._g, self._p, self._sig, self.s1, self.s2,
+                                    self.absmax1, self.absmax2, self.n_pad, self.grads.dtype, step=self.t,
+                                    epoch=self.epoch, num_ctas=self.num_ctas, hp=self.hp)
