@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-zero1", action="store_true", help="run the ZeRO-1 round trip even at one rank")
+    ap.add_argument("--zero-fused", action="store_true",
+                    help="also time the fused ZeRO-1 kernel (peer-memory RS + step + AG in one launch)")
     return ap.parse_args()
 
 
@@ -380,6 +382,26 @@ def main():
                  "all_gather_bytes_per_rank": n_pad * 4, "backend": "nccl", "steps": args.zero1_steps}
         del zo
         torch.cuda.empty_cache()
+        if args.zero_fused:
+            zf = zero.ZeroFusedOptimizer8bit(n_total, kind=kind, grad_dtype=TORCH_DT[gdt], device=dev, **hp)
+            zf.params[:n_total].normal_(0, 0.02)
+            zf.grads[:n_total].normal_(0, 1e-3)
+            for _ in range(2):
+                zf.step()
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(args.zero1_steps):
+                zf.step()
+            b.record()
+            torch.cuda.synchronize()
+            zt = torch.tensor([a.elapsed_time(b) / args.zero1_steps], dtype=torch.float64, device=dev)
+            dist.all_reduce(zt, op=dist.ReduceOp.MAX)
+            zero1["fused"] = {"ms_per_step": float(zt[0]), "params_per_s": n_total / (float(zt[0]) / 1e3),
+                              "kernel": "optim8bit_step_kernel MODE_ZERO (peer loads + step + peer stores)"}
+            del zf
+            torch.cuda.empty_cache()
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
