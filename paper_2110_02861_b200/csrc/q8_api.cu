@@ -549,7 +549,7 @@ int64_t q8_layerwise_workspace_bytes(const q8_tensor* tensors_host, int32_t num_
     if (num_tensors < 0 || (num_tensors > 0 && !tensors_host)) return -1;
     for (int32_t i = 0; i < num_tensors; ++i)
         if (tensors_host[i].n < 0) return -1;
-    return lw_scale_bytes(num_tensors) + 16 * lw_partial_blocks(tensors_host, num_tensors);
+    return lw_scale_bytes(num_tensors) + 16 * q8::kNormSlots * lw_partial_blocks(tensors_host, num_tensors);
 }
 
 q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_tensor* tensors_host,

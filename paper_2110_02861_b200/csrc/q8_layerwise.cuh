@@ -16,6 +16,7 @@
 #pragma once
 
 #include "q8_kernels.cuh"
+#include "q8_step_kernel.cuh"
 
 namespace q8 {
 
@@ -29,7 +30,7 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
 // norms pass needs the full dequantize + update and runs in the fused step kernel's MODE_NORMS.
 template <int GDT, int MAXT>
 __global__ void __launch_bounds__(kThreads) lars_norms_kernel(const __grid_constant__ StepParams<MAXT> P) {
-    __shared__ double red[2][kWarps];
+    static_assert(kWarps == kNormSlots, "one partial slot per warp");
     const int tid = threadIdx.x;
     int ti = 0;
     for (int64_t gb = blockIdx.x; gb < P.total_blocks; gb += gridDim.x) {
@@ -62,39 +63,36 @@ __global__ void __launch_bounds__(kThreads) lars_norms_kernel(const __grid_const
         }
         sw = warp_sum_f64(sw);
         sg = warp_sum_f64(sg);
-        if ((tid & 31) == 0) {
-            red[0][tid >> 5] = sw;
-            red[1][tid >> 5] = sg;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            double a = 0.0, x = 0.0;
-            for (int k = 0; k < kWarps; ++k) {
-                a += red[0][k];
-                x += red[1][k];
-            }
-            P.partial[gb] = make_double2(a, x);
-        }
-        __syncthreads();
+        if ((tid & 31) == 0) P.partial[gb * kNormSlots + (tid >> 5)] = make_double2(sw, sg);
     }
 }
 
-// One CTA (kThreads) per tensor of the launch: ||w|| and ||x|| from its block partials (fixed
-// summation order: thread-strided, warp butterfly, warps in order), then the fp32 scale (L1-L3):
+// One CTA (kThreads) per tensor of the launch: ||w|| and ||x|| from its per-warp block partials
+// (wpb of the kNormSlots slots per block; fixed summation order: thread-strided over blocks, slots in
+// order, warp butterfly, warps in order), then the fp32 scale (L1-L3):
 //   LAMB  a = RN(lr * (||w|| / ||u||))                    (1 when either norm is 0)
 //   LARS  a = RN(lr * (eta ||w|| / (||g|| + wd ||w||)))   (lr when either norm is 0)
+constexpr int kScaleThreads = 1024;
 template <int KIND, int MAXT>
-__global__ void __launch_bounds__(kThreads) layer_scale_kernel(const __grid_constant__ StepParams<MAXT> P,
-                                                               const double2* __restrict__ partial,
-                                                               float* __restrict__ scale, double lr, double eta,
-                                                               double wd) {
-    __shared__ double red[2][kWarps];
+__global__ void __launch_bounds__(kScaleThreads) layer_scale_kernel(const __grid_constant__ StepParams<MAXT> P,
+                                                                    const double2* __restrict__ partial,
+                                                                    float* __restrict__ scale, double lr, double eta,
+                                                                    double wd, int wpb) {
+    __shared__ double red[2][kScaleThreads / 32];
     const int t = blockIdx.x, tid = threadIdx.x;
     double sw = 0.0, sx = 0.0;
-    for (int64_t b = P.block_start[t] + tid; b < P.block_start[t + 1]; b += kThreads) {
-        const double2 v = partial[b];
-        sw += v.x;
-        sx += v.y;
+    const int64_t b1 = P.block_start[t + 1];
+    for (int64_t b = P.block_start[t] + tid; b < b1; b += kScaleThreads) {
+        double2 v[kNormSlots];
+#pragma unroll
+        for (int k = 0; k < kNormSlots; ++k)  // independent loads first, then the sums in slot order
+            if (k < wpb) v[k] = partial[b * kNormSlots + k];
+#pragma unroll
+        for (int k = 0; k < kNormSlots; ++k)
+            if (k < wpb) {
+                sw += v[k].x;
+                sx += v[k].y;
+            }
     }
     sw = warp_sum_f64(sw);
     sx = warp_sum_f64(sx);
@@ -105,7 +103,7 @@ __global__ void __launch_bounds__(kThreads) layer_scale_kernel(const __grid_cons
     __syncthreads();
     if (tid == 0) {
         sw = sx = 0.0;
-        for (int k = 0; k < kWarps; ++k) {
+        for (int k = 0; k < kScaleThreads / 32; ++k) {
             sw += red[0][k];
             sx += red[1][k];
         }

@@ -70,7 +70,8 @@ cudaError_t launch_layerwise_t(const StepParams<kMultiMaxT>& P, const LaunchCtx&
     constexpr int NS = G == G_F32 ? 3 : 4;
     constexpr int SUBT = G == G_F32 ? 256 : 128;
     if (P.total_blocks == 0) {  // only empty tensors: their scale is still defined (lr)
-        layer_scale_kernel<KIND, kMultiMaxT><<<P.num_tensors, kThreads, 0, ctx.stream>>>(P, partial, scale, lr, eta, wd);
+        layer_scale_kernel<KIND, kMultiMaxT><<<P.num_tensors, kScaleThreads, 0, ctx.stream>>>(P, partial, scale, lr, eta, wd,
+                                                                                        0);
         return cudaGetLastError();
     }
     cudaError_t e;
@@ -90,7 +91,10 @@ cudaError_t launch_layerwise_t(const StepParams<kMultiMaxT>& P, const LaunchCtx&
         e = cudaGetLastError();
     }
     if (e != cudaSuccess) return e;
-    layer_scale_kernel<KIND, kMultiMaxT><<<P.num_tensors, kThreads, 0, ctx.stream>>>(P, partial, scale, lr, eta, wd);
+    // partial slots written per block: the step kernel's warps per sub-block (LAMB) or 8 (LARS)
+    const int wpb = KIND == KIND_LAMB ? SUBT / 32 : kWarps;
+    layer_scale_kernel<KIND, kMultiMaxT><<<P.num_tensors, kScaleThreads, 0, ctx.stream>>>(P, partial, scale, lr, eta, wd,
+                                                                                    wpb);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     return persistent(optim8bit_step_kernel<KIND, G, kMultiMaxT, SEARCH_BUCKET, NS, SUBT>, NS, SUBT, P.total_blocks,
