@@ -214,3 +214,43 @@ def optim8bit_layerwise_step(kind, p, g, s1, s2, absmax1, absmax2, *, lr, beta1=
     if rc != 0:
         raise ValueError("invalid arguments")
     return out[0]
+
+
+def _quantile_lib():
+    l = lib()
+    if not getattr(l, "_quantiles_bound", False):
+        f32p = ctypes.POINTER(ctypes.c_float)
+        l.oracle_exact_quantiles.argtypes = [f32p, ctypes.c_int64, f32p]
+        l.oracle_sram_quantiles.argtypes = [f32p, ctypes.c_int64, ctypes.c_int64, f32p]
+        l.oracle_quantile_codebook.argtypes = [f32p, f32p]
+        l._quantiles_bound = True
+    return l
+
+
+def exact_quantiles(x: np.ndarray) -> np.ndarray:
+    """Sample quantiles Q(j/257), j = 0..256, of the whole tensor (App G; readings Q1, Q2)."""
+    x = _f32(x).ravel()
+    out = np.zeros(257, np.float32)
+    if _quantile_lib().oracle_exact_quantiles(_ptr(x, ctypes.c_float), x.size, _ptr(out, ctypes.c_float)) != 0:
+        raise ValueError("invalid arguments")
+    return out
+
+
+def sram_quantiles(x: np.ndarray, subset: int = 4096) -> np.ndarray:
+    """SRAM-Quantiles (App G; readings Q1-Q4): per-chunk sample quantiles, averaged."""
+    x = _f32(x).ravel()
+    out = np.zeros(257, np.float32)
+    if _quantile_lib().oracle_sram_quantiles(_ptr(x, ctypes.c_float), x.size, int(subset),
+                                             _ptr(out, ctypes.c_float)) != 0:
+        raise ValueError("invalid arguments")
+    return out
+
+
+def quantile_codebook(quantiles: np.ndarray) -> np.ndarray:
+    """Quantile data type from 257 quantiles (Eq.5, reading Q5): 256 values in [-1, 1]."""
+    q = _f32(quantiles)
+    assert q.size == 257
+    out = np.zeros(256, np.float32)
+    if _quantile_lib().oracle_quantile_codebook(_ptr(q, ctypes.c_float), _ptr(out, ctypes.c_float)) != 0:
+        raise ValueError("all Eq.5 midpoints are zero")
+    return out

@@ -37,6 +37,13 @@
  *   oracle_optim8bit_layerwise_step   pinned: == dequantize -> 32-bit layer-wise step
  *                              -> block quantize (bit-exact), 8-bit vs 32-bit within
  *                              quantization error
+ *   oracle_exact_quantiles    pinned: closed-form order statistics of permuted integer
+ *                              ranges, np.sort indexing, scipy normal ppf (large n)
+ *   oracle_sram_quantiles     pinned: == exact quantiles when one chunk holds the tensor;
+ *                              constant chunks -> their mean (closed form); permutation
+ *                              invariance inside a chunk; close to the normal ppf
+ *   oracle_quantile_codebook  pinned: uniform data -> evenly spaced Eq.5 midpoints (closed
+ *                              form); symmetry for symmetric quantiles; max |code| = 1
  */
 #include <math.h>
 #include <pthread.h>
@@ -441,4 +448,85 @@ int oracle_optim8bit_layerwise_step(int kind, float* p, const float* g, uint8_t*
     free(m);
     free(r);
     return rc;
+}
+
+/* ------------------------------------------------------------------------- */
+/* 7. Quantile quantization (App F.2, Eq.5) and SRAM-Quantiles      */
+/*    (App G)                                                        */
+/* ------------------------------------------------------------------------- */
+
+/*
+ * Readings (rows Q1-Q5):
+ *  Q1  Eq.5: q_i = (Q_X(i/(2^k+1)) + Q_X((i+1)/(2^k+1))) / 2, i = 0..2^k-1, so k = 8
+ *      needs the 257 quantiles Q_X(j/257), j = 0..256, as the equation is written (the prose
+ *      "2^k+1 equally spaced quantiles over [0,1]" would put them at j/256; we follow the formula).
+ *  Q2  sample quantile: "the value at index i = q x n" of the ascending sorted values,
+ *      0-based, i = floor(j*m/257) computed exactly in integers for a set of m values.
+ *  Q3  SRAM-Quantiles subsets: consecutive chunks of S values ("about 4096 32-bit
+ *      values"), the last one possibly short; each chunk's quantiles are found from its own
+ *      eCDF (Q2 with its own m).
+ *  Q4  "we average the quantiles": arithmetic mean over chunks, every chunk weight 1,
+ *      summed in binary64 and rounded once to binary32.  (The paper's atomic averaging has no
+ *      fixed order; the oracle sums in chunk order.)
+ *  Q5  Eq.5 midpoints in binary64, normalized into [-1, 1] by their largest magnitude (Fig. 6
+ *      caption P:427 "normalize them into the range [-1, 1]"), rounded once to binary32.
+ */
+
+static int cmp_float_total(const void* a, const void* b) {
+    /* ascending by value; -0 before +0 so the order is total (only relevant for the bit of a zero) */
+    float x = *(const float*)a, y = *(const float*)b;
+    if (x < y) return -1;
+    if (x > y) return 1;
+    return (signbit(y) != 0) - (signbit(x) != 0);
+}
+
+/* Q2 on one set of m values: sort a copy, take index floor(j*m/257) for j = 0..256. */
+static void sample_quantiles(const float* x, int64_t m, float* tmp, float out[257]) {
+    memcpy(tmp, x, sizeof(float) * (size_t)m);
+    qsort(tmp, (size_t)m, sizeof(float), cmp_float_total);
+    for (int64_t j = 0; j <= 256; j++) out[j] = tmp[(j * m) / 257];
+}
+
+/* The exact sample quantiles of the whole tensor ("The easiest way to find the eCDF is
+ * to sort a given tensor"): Q2 with m = n.  n >= 1. */
+int oracle_exact_quantiles(const float* x, int64_t n, float out[257]) {
+    if (n < 1) return -1;
+    float* tmp = (float*)malloc(sizeof(float) * (size_t)n);
+    if (!tmp) return -1;
+    sample_quantiles(x, n, tmp, out);
+    free(tmp);
+    return 0;
+}
+
+/* SRAM-Quantiles (App G): the quantiles of every S-value chunk (Q3), averaged (Q4).
+ * out[j] estimates Q_X(j/257), j = 0..256.  n >= 1, S >= 1. */
+int oracle_sram_quantiles(const float* x, int64_t n, int64_t S, float out[257]) {
+    if (n < 1 || S < 1) return -1;
+    int64_t nchunks = (n + S - 1) / S;
+    float* tmp = (float*)malloc(sizeof(float) * (size_t)S);
+    if (!tmp) return -1;
+    double sum[257];
+    float q[257];
+    for (int j = 0; j <= 256; j++) sum[j] = 0.0;
+    for (int64_t c = 0; c < nchunks; c++) {
+        int64_t start = c * S, m = (n - start < S) ? n - start : S;
+        sample_quantiles(x + start, m, tmp, q);
+        for (int j = 0; j <= 256; j++) sum[j] += (double)q[j];
+    }
+    for (int j = 0; j <= 256; j++) out[j] = (float)(sum[j] / (double)nchunks);
+    free(tmp);
+    return 0;
+}
+
+/* Quantile data type (Eq.5, Q1/Q5) from the 257 quantiles Q_X(j/257): 256 values in [-1, 1],
+ * ascending whenever the quantiles are.  Returns -1 if every midpoint is 0 (no scale). */
+int oracle_quantile_codebook(const float quantiles[257], float out[256]) {
+    double mid[256], M = 0.0;
+    for (int i = 0; i < 256; i++) {
+        mid[i] = ((double)quantiles[i] + (double)quantiles[i + 1]) * 0.5;
+        if (fabs(mid[i]) > M) M = fabs(mid[i]);
+    }
+    if (!(M > 0.0)) return -1;
+    for (int i = 0; i < 256; i++) out[i] = (float)(mid[i] / M);
+    return 0;
 }
