@@ -246,6 +246,8 @@ def main():
     cfg = workload_config(args.workload, world)
     if synth.WORKLOADS[args.workload].get("layerwise"):
         return main_layerwise(args, cfg, q8, world, rank, local, dev)
+    if synth.WORKLOADS[args.workload].get("quantiles"):
+        return main_quantiles(args, cfg, q8, world, rank, local, dev)
     kind, gdt = cfg["kind"], cfg["grad_dtype"]
     hp = dict(cfg["hparams"])
     n_total = cfg["n_params"]
@@ -563,6 +565,80 @@ def main_layerwise(args, cfg, q8, world, rank, local, dev):
                          else "fallback 6.65 TB/s (B200_PROFILING.md)"},
             "cpu_baseline": cpu_baseline, "e2e": None, "gpu_launches": args.steps * 3 * chunks,
             "clocks": clk.summary(), "library": q8.version(),
+        }))
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+def main_quantiles(args, cfg, q8, world, rank, local, dev):
+    """SRAM-Quantiles (App G): the 257 quantiles of a GPT-2-XL-sized fp32
+    buffer (the parameters, N(0, 0.02^2)) plus the Eq.5 codebook; a step is one
+    q8_estimate_quantiles call (sort/accumulate pass + finalize).  Independent problems per GPU
+    (weak scaling replicas).  The roofline is the ALU issue rate: the kernel sorts every 4096-value
+    chunk on chip with a 78-stage bitonic network (one min-or-max per key per stage)."""
+    n = cfg["n_params"]
+    x = synth.params(n, seed=1 + rank, device=dev)
+    ws = torch.empty(q8.quantiles_workspace_bytes(n), dtype=torch.uint8, device=dev)
+    qout = torch.empty(257, dtype=torch.float32, device=dev)
+    code = torch.empty(256, dtype=torch.float32, device=dev)
+
+    def one():
+        q8.estimate_quantiles(x, with_codebook=True, workspace=ws, quantiles=qout, code=code)
+
+    for _ in range(args.warmup):
+        one()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            one()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    ms = torch.tensor([statistics.mean(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_per_step = float(ms[0])
+    clocks = clk.summary()
+    sm_max = clocks.get("sm_max_mhz") or 1965.0
+    ops_per_elem = 78  # bitonic stages for 4096 keys: 12*13/2, one min-or-max per key per stage
+    # min/max (IMNMX) issue on the ALU pipe: rt_SMSP = 2 cycles per warp instruction (B300_MICROARCH.md
+    # "Pipe rates"), i.e. 16 lanes/clk per SMSP, 64 per SM; 148 SMs (B200_PROFILING.md)
+    peak_ops = 148 * 4 * 16 * sm_max * 1e6 / 1e12
+    achieved = n * ops_per_elem / (ms_per_step / 1e3) / 1e12
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        m = 1 << 25
+        xs = x[:m].cpu().numpy()
+        t0 = time.perf_counter()
+        oracle.sram_quantiles(xs)
+        dt = time.perf_counter() - t0
+        cpu_baseline = {"value": m / dt, "unit": "elements/s", "cores": 1, "kind": "oracle",
+                        "sample": f"the first {m:,} elements ({m // 4096:,} chunks) of the buffer, 1 thread, {dt:.1f} s"}
+    if rank == 0:
+        cfg = {"workload": cfg["workload"], "n_elements": n, "chunk": 4096, "quantiles": 257,
+               "parallelism": f"replicas-{world}" if world > 1 else "single-gpu",
+               "l2": "inputs (6.2 GB) exceed the 126 MB L2; no flush between steps"}
+        print(json.dumps({
+            "metric": "SRAM-Quantiles elements/sec (App G)", "value": world * n / (ms_per_step / 1e3),
+            "unit": "elements/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "ns_per_element": ms_per_step * 1e6 / n, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "paper_context": "0.064 ns/element (App G P:444; GPU not stated)",
+            "data": "synthetic: x ~ N(0, 0.02^2) fp32 (the GPT-2-XL-sized parameter buffer)",
+            "config": cfg,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_ops, "unit": "Tops/s",
+                         "frac": achieved / peak_ops, "traffic": None, "ops_per_element": ops_per_elem,
+                         "kernel": "sram_quantiles_kernel (+ one-CTA finalize)",
+                         "peak_source": "ALU pipe: 148 SMs x 4 SMSPs x 16 lanes/clk (rt_SMSP=2) x sm_max clock",
+                         "hbm_gbs": n * 4 / (ms_per_step / 1e3) / 1e9},
+            "cpu_baseline": cpu_baseline, "e2e": None, "gpu_launches": args.steps * 2,
+            "clocks": clocks, "library": q8.version(),
         }))
     if dist.is_initialized():
         dist.destroy_process_group()

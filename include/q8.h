@@ -126,6 +126,35 @@ q8_status q8_quantize_tensorwise(const float* code_dev, const float* x_dev, floa
 q8_status q8_dequantize_tensorwise(const float* code_dev, const uint8_t* codes_dev, const float* absmax_dev,
                                    float* out_dev, int64_t n, void* stream);
 
+/* SRAM-Quantiles (App G): approximate sample quantiles Q_X(j/257), j = 0..256, of the
+ * tensor x -- the 257 quantiles whose Eq.5 midpoints form the quantile data type (App F.2,
+ * P:403-416).  "we find the eCDF for a subset of values of the tensor that fits into SRAM (about
+ * 4096 32-bit values).  Once we found the quantiles for each subset, we average the quantiles"
+ * (P:440).  Readings Q1-Q4: chunks of 4096 consecutive elements (the last may be
+ * short), each sorted on chip; chunk quantile j = its sorted value at index floor(j*m/257);
+ * the estimate is the mean over chunks, accumulated in binary64 and rounded once to fp32 (the
+ * summation order is fixed per device -- deterministic -- but differs from a sequential sum).
+ *   x_dev          [n] fp32, 16-B aligned (read); n >= 1 (else INVALID).  NaNs are out of contract.
+ *   quantiles_dev  [257] fp32 (written)
+ *   code_dev       NULL, or [256] fp32 (written): the quantile data type of Eq.5 (reading Q5),
+ *                  RN32(mid_i / max|mid|) with mid_i = (Q_i + Q_{i+1})/2 in binary64 (all zeros if
+ *                  every midpoint is 0), usable as code_dev of q8_quantize_blockwise (entries are
+ *                  non-decreasing; equal neighbours resolve to the lower index)
+ *   workspace_dev  >= q8_quantiles_workspace_bytes(n) bytes, 16-B aligned, caller-owned scratch
+ *                  (binary64 partial sums per CTA), not shared with a concurrent call
+ * Two stream-ordered launches: the sort/accumulate pass and a one-CTA finalize. */
+q8_status q8_estimate_quantiles(const float* x_dev, int64_t n, float* quantiles_dev, float* code_dev,
+                                void* workspace_dev, int64_t workspace_bytes, void* stream);
+
+/* Bytes of workspace q8_estimate_quantiles needs for n elements on the current device (host
+ * function): 257 * 8 per persistent CTA.  -1 on bad input or no device. */
+int64_t q8_quantiles_workspace_bytes(int64_t n);
+
+/* Quantile data type from 257 host quantiles (Eq.5, reading Q5): out_host[i] =
+ * RN32(mid_i / max_k |mid_k|), mid_i = (q_i + q_{i+1})/2 in binary64.  Pure host function.
+ * Errors: INVALID for NULL buffers or when every midpoint is 0. */
+q8_status q8_create_quantile_codebook(const float* quantiles_host, float* out_host);
+
 /* The fused 8-bit optimizer step (S3; Fig.1), in place, for one tensor:
  * for each block b:
  *   1. dequantize  m = Q_s[s1_i] * absmax1[b],  r = Q_u[s2_i] * absmax2[b]

@@ -26,7 +26,8 @@ EXPORTS = ("q8_create_dynamic_codebook", "q8_create_linear_codebook", "q8_quanti
            "q8_dequantize_tensorwise",
            "q8_optim8bit_step", "q8_optim8bit_step_multi", "q8_optim32bit_step_multi",
            "q8_optim8bit_step_layerwise", "q8_layerwise_workspace_bytes", "q8_optim8bit_step_zero_fused",
-           "q8_zero_signal_bytes", "q8_last_error", "q8_version")
+           "q8_zero_signal_bytes", "q8_estimate_quantiles", "q8_quantiles_workspace_bytes",
+           "q8_create_quantile_codebook", "q8_last_error", "q8_version")
 
 
 class Q8Error(RuntimeError):
@@ -74,10 +75,14 @@ def _load():
                                                  ctypes.POINTER(vp), vp, vp, vp, vp, i64, i32, ctypes.POINTER(HParams),
                                                  i64, ctypes.c_uint32, i32, vp]
     lib.q8_zero_signal_bytes.argtypes = [i32, i32]
+    lib.q8_estimate_quantiles.argtypes = [vp, i64, vp, vp, vp, i64, vp]
+    lib.q8_quantiles_workspace_bytes.argtypes = [i64]
+    lib.q8_create_quantile_codebook.argtypes = [vp, vp]
     for f in EXPORTS[:-2]:
         getattr(lib, f).restype = ctypes.c_int
     lib.q8_layerwise_workspace_bytes.restype = i64
     lib.q8_zero_signal_bytes.restype = i64
+    lib.q8_quantiles_workspace_bytes.restype = i64
     lib.q8_last_error.restype = ctypes.c_char_p
     lib.q8_version.restype = ctypes.c_char_p
     return lib
@@ -340,3 +345,42 @@ def optim8bit_step_zero_fused(kind, world, rank, g_ptrs, p_ptrs, sig_ptrs, s1, s
                                             _dev_ptr(absmax2, torch.float32, "absmax2"), int(n_pad), BLOCKSIZE,
                                             ctypes.byref(hp), int(step), int(epoch), int(num_ctas),
                                             stream if stream is not None else _stream(s1.device)))
+
+
+def quantiles_workspace_bytes(n: int) -> int:
+    nb = lib.q8_quantiles_workspace_bytes(int(n))
+    if nb < 0:
+        raise Q8Error(Q8_ERR_INVALID, lib.q8_last_error().decode() or "invalid n")
+    return nb
+
+
+def estimate_quantiles(x: torch.Tensor, *, with_codebook: bool = False, workspace: torch.Tensor | None = None,
+                       quantiles: torch.Tensor | None = None, code: torch.Tensor | None = None):
+    """SRAM-Quantiles (App G): the 257 quantiles Q(j/257) of x (fp32, on the GPU).  With
+    with_codebook, also the Eq.5 quantile data type (256 fp32 in [-1, 1], on the GPU), usable
+    as the `code` table of quantize_blockwise.  Returns quantiles or (quantiles, code)."""
+    n = x.numel()
+    need = quantiles_workspace_bytes(n)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+    if quantiles is None:
+        quantiles = torch.empty(257, dtype=torch.float32, device=x.device)
+    if with_codebook and code is None:
+        code = torch.empty(256, dtype=torch.float32, device=x.device)
+    if quantiles.numel() != 257 or (code is not None and code.numel() != 256):
+        raise ValueError("size mismatch")
+    _check(lib.q8_estimate_quantiles(_dev_ptr(x, torch.float32, "x"), n, _dev_ptr(quantiles, torch.float32, "quantiles"),
+                                     _dev_ptr(code, torch.float32, "code") if with_codebook else None,
+                                     _dev_ptr(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                     _stream(x.device)))
+    return (quantiles, code) if with_codebook else quantiles
+
+
+def create_quantile_codebook(quantiles) -> torch.Tensor:
+    """Host call: the Eq.5 quantile data type from 257 quantiles (reading Q5)."""
+    q = torch.as_tensor(quantiles, dtype=torch.float32).detach().cpu().contiguous()
+    if q.numel() != 257:
+        raise ValueError("need 257 quantiles")
+    out = torch.empty(256, dtype=torch.float32)
+    _check(lib.q8_create_quantile_codebook(q.data_ptr(), out.data_ptr()))
+    return out

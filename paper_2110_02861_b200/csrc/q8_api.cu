@@ -16,6 +16,7 @@
 #include "q8_launch.h"
 #include "q8_step_kernel.cuh"
 #include "q8_step32_kernel.cuh"
+#include "q8_quantiles.cuh"
 
 namespace q8 {
 void build_dynamic_codebook(bool is_signed, float out[256]);
@@ -265,6 +266,71 @@ q8_status q8_create_linear_codebook(int32_t is_signed, float* out_host) {
         const double v = is_signed ? -1.0 + 2.0 * static_cast<double>(i) / 255.0 : static_cast<double>(i) / 255.0;
         out_host[i] = static_cast<float>(v);
     }
+    return ok();
+}
+
+// ---------------------------------------------------------------- SRAM-Quantiles (App G)
+namespace {
+int quantile_rows(const DeviceState* d, int64_t nchunks) {
+    static int occ = [] {
+        int o = 0;
+        if (q8::ensure_smem(reinterpret_cast<const void*>(q8::sram_quantiles_kernel), q8::kQSmemBytes) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, q8::sram_quantiles_kernel, q8::kQThreads,
+                                                          q8::kQSmemBytes) != cudaSuccess || o < 1)
+            o = 1;
+        const char* env = std::getenv("Q8_QUANTILE_CTAS_PER_SM");
+        if (env && std::atoi(env) > 0) o = std::atoi(env);
+        return o;
+    }();
+    return static_cast<int>(grid_for(d, occ, nchunks));
+}
+}  // namespace
+
+int64_t q8_quantiles_workspace_bytes(int64_t n) {
+    if (n < 1) return -1;
+    DeviceState* d = nullptr;
+    if (device_state(&d) != Q8_OK) return -1;
+    const int64_t nchunks = (n + q8::kQChunk - 1) / q8::kQChunk;
+    return static_cast<int64_t>(quantile_rows(d, nchunks)) * q8::kQuantiles * static_cast<int64_t>(sizeof(double));
+}
+
+q8_status q8_estimate_quantiles(const float* x_dev, int64_t n, float* quantiles_dev, float* code_dev,
+                                void* workspace_dev, int64_t workspace_bytes, void* stream) {
+    if (n < 1) return fail(Q8_ERR_INVALID, "n must be >= 1 (quantiles of an empty tensor are undefined)");
+    if (!x_dev || !quantiles_dev || !workspace_dev) return fail(Q8_ERR_INVALID, "NULL buffer");
+    if (!aligned(x_dev, 16) || !aligned(workspace_dev, 16) || !aligned(quantiles_dev, 4) ||
+        (code_dev && !aligned(code_dev, 4)))
+        return fail(Q8_ERR_INVALID, "misaligned buffer (x and workspace 16 B)");
+    DeviceState* d = nullptr;
+    if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    const int64_t nchunks = (n + q8::kQChunk - 1) / q8::kQChunk;
+    const int rows = quantile_rows(d, nchunks);
+    const int64_t need = static_cast<int64_t>(rows) * q8::kQuantiles * static_cast<int64_t>(sizeof(double));
+    if (workspace_bytes < need)
+        return fail(Q8_ERR_INVALID, "workspace too small: %lld < %lld bytes", static_cast<long long>(workspace_bytes),
+                    static_cast<long long>(need));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    double* partial = static_cast<double*>(workspace_dev);
+    q8::sram_quantiles_kernel<<<rows, q8::kQThreads, q8::kQSmemBytes, st>>>(x_dev, n, nchunks, partial);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "sram_quantiles_kernel launch");
+    q8::quantiles_finalize_kernel<<<1, 288, 0, st>>>(partial, rows, nchunks, quantiles_dev, code_dev);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "quantiles_finalize_kernel launch");
+    return ok();
+}
+
+q8_status q8_create_quantile_codebook(const float* quantiles_host, float* out_host) {
+    if (!quantiles_host || !out_host) return fail(Q8_ERR_INVALID, "NULL buffer");
+    // Eq.5: midpoints of consecutive quantiles, in double; normalized into [-1, 1] by the
+    // largest magnitude (Fig. 6 caption), rounded once (reading Q5)
+    double mid[256], M = 0.0;
+    for (int i = 0; i < 256; ++i) {
+        mid[i] = (static_cast<double>(quantiles_host[i]) + static_cast<double>(quantiles_host[i + 1])) * 0.5;
+        M = std::max(M, std::fabs(mid[i]));
+    }
+    if (!(M > 0.0) || !std::isfinite(M)) return fail(Q8_ERR_INVALID, "every Eq.5 midpoint is zero (or non-finite)");
+    for (int i = 0; i < 256; ++i) out_host[i] = static_cast<float>(mid[i] / M);
     return ok();
 }
 

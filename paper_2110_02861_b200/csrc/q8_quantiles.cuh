@@ -1,0 +1,229 @@
+// q8_quantiles.cuh -- SRAM-Quantiles (App G) and the quantile data type (App F.2,
+// Eq.5) on sm_100a.  Readings Q1-Q5 in DESIGN.md section 3.
+//
+// "Instead of finding the full eCDF we find the eCDF for a subset of values of the tensor that
+// fits into SRAM (about 4096 32-bit values).  Once we found the quantiles for each subset, we
+// average the quantiles".  B200 design:
+//   * persistent CTAs of 256 threads, each chunk of 4096 values sorted entirely on chip: 16 keys
+//     per thread in registers, a bitonic network in its "flip" form (every comparator ascending:
+//     for each merge size K a mirror stage e <-> e^(K-1), then half-cleaners e <-> e^j), so no
+//     per-stage direction logic.  Comparators whose partners live in the same thread are
+//     register min/max; partners in the same warp are exchanged with SHFL (j = 16..256); only
+//     the 6 stages with partners in another warp (j >= 512) go through shared memory, double-
+//     buffered so each needs one barrier.  Keys are the monotone unsigned image of the fp32 bits.
+//   * the 257 order statistics floor(j*m/257) (Q1, Q2) are read from the sorted chunk and summed
+//     per thread in binary64 registers across the CTA's chunks (Q4); one partial row per CTA.
+//   * a one-CTA finalize kernel sums the partial rows in CTA order, divides by the chunk count,
+//     rounds once to fp32, and optionally builds the Eq.5 codebook (Q5) on the device.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace q8 {
+
+constexpr int kQChunk = 4096;          // "about 4096 32-bit values", reading Q3
+constexpr int kQThreads = 256;
+constexpr int kQPer = kQChunk / kQThreads;  // 16 keys per thread
+constexpr int kQuantiles = 257;        // Q_X(j/257), j = 0..256 (Eq.5, reading Q1)
+constexpr int kQSmemBytes = 2 * kQChunk * 4;  // two 16 KB exchange buffers
+
+// monotone unsigned key of an fp32 value (total order, -0 < +0) and back
+__device__ __forceinline__ uint32_t qkey(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return b ^ (static_cast<uint32_t>(static_cast<int32_t>(b) >> 31) | 0x80000000u);
+}
+__device__ __forceinline__ float qval(uint32_t k) {
+    return __uint_as_float(k ^ ((k >> 31) ? 0x80000000u : 0xffffffffu));
+}
+
+// word offset of key e = 16 t + r in an exchange buffer: thread t's four quads are permuted by
+// (t >> 1) & 3 so eight consecutive threads' 16-byte accesses hit eight distinct bank groups
+__device__ __forceinline__ int qslot(int t, int q) { return 16 * t + 4 * (q ^ ((t >> 1) & 3)); }
+
+// ------------------------------------------------------------------ comparator stages
+// in-thread half-cleaner, distance J in {1, 2, 4, 8}
+template <int J>
+__device__ __forceinline__ void q_ce_reg(uint32_t (&a)[kQPer]) {
+#pragma unroll
+    for (int r = 0; r < kQPer; r++)
+        if (!(r & J)) {
+            const uint32_t x = a[r], y = a[r | J];
+            a[r] = min(x, y);
+            a[r | J] = max(x, y);
+        }
+}
+
+// in-thread mirror stage of merge size K in {2, 4, 8, 16}: r <-> r ^ (K-1)
+template <int K>
+__device__ __forceinline__ void q_mirror_reg(uint32_t (&a)[kQPer]) {
+#pragma unroll
+    for (int r = 0; r < kQPer; r++)
+        if (!(r & (K / 2))) {
+            const int p = r ^ (K - 1);
+            const uint32_t x = a[r], y = a[p];
+            a[r] = min(x, y);
+            a[p] = max(x, y);
+        }
+}
+
+// warp half-cleaner: partner lane ^ M (M in 1..16), same register; the lower thread keeps min
+template <int M>
+__device__ __forceinline__ void q_ce_shfl(uint32_t (&a)[kQPer], int lane) {
+    const bool lower = !(lane & M);
+#pragma unroll
+    for (int r = 0; r < kQPer; r++) {
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, a[r], M);
+        a[r] = lower ? min(a[r], o) : max(a[r], o);
+    }
+}
+
+// warp mirror stage of merge size K in {32..512}: partner lane ^ (K/16 - 1), register 15 - r
+template <int K>
+__device__ __forceinline__ void q_mirror_shfl(uint32_t (&a)[kQPer], int lane) {
+    constexpr int M = K / 16 - 1;
+    const bool lower = !(lane & (K / 32));
+    uint32_t o[kQPer];
+#pragma unroll
+    for (int r = 0; r < kQPer; r++) o[r] = __shfl_xor_sync(0xffffffffu, a[kQPer - 1 - r], M);
+#pragma unroll
+    for (int r = 0; r < kQPer; r++) a[r] = lower ? min(a[r], o[r]) : max(a[r], o[r]);
+}
+
+// cross-warp stage through shared memory: partner thread t ^ T; MIRROR reverses the registers
+// (mirror of merge size K: T = K/16 - 1, lower bit K/32).  `buf` alternates between the two
+// exchange buffers, so one barrier per stage suffices (a buffer is rewritten only after the
+// next stage's barrier, which every thread reaches after its reads of this one).
+template <int T, bool MIRROR>
+__device__ __forceinline__ void q_stage_smem(uint32_t (&a)[kQPer], int t, uint32_t* xbuf, int& buf) {
+    uint32_t* s = xbuf + buf * kQChunk;
+    buf ^= 1;
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+        *reinterpret_cast<uint4*>(s + qslot(t, q)) = make_uint4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+    __syncthreads();
+    const int pt = t ^ T;
+    const bool lower = MIRROR ? !(t & ((T + 1) / 2)) : !(t & T);
+    uint32_t o[kQPer];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const uint4 v = *reinterpret_cast<const uint4*>(s + qslot(pt, q));
+        o[4 * q] = v.x;
+        o[4 * q + 1] = v.y;
+        o[4 * q + 2] = v.z;
+        o[4 * q + 3] = v.w;
+    }
+#pragma unroll
+    for (int r = 0; r < kQPer; r++) {
+        const uint32_t p = MIRROR ? o[kQPer - 1 - r] : o[r];
+        a[r] = lower ? min(a[r], p) : max(a[r], p);
+    }
+}
+
+// half-cleaners of distance J, J/2, ..., 1 (key e = 16 t + r: J < 16 in registers, J < 512
+// within the warp, else shared memory)
+template <int J>
+__device__ __forceinline__ void q_cleaners(uint32_t (&a)[kQPer], int t, int lane, uint32_t* xbuf, int& buf) {
+    if constexpr (J >= 1) {
+        if constexpr (J < 16) q_ce_reg<J>(a);
+        else if constexpr (J < 512) q_ce_shfl<J / 16>(a, lane);
+        else q_stage_smem<J / 16, false>(a, t, xbuf, buf);
+        q_cleaners<J / 2>(a, t, lane, xbuf, buf);
+    }
+}
+
+// bitonic merges of size K, 2K, ..., 4096 (flip form: mirror stage, then half-cleaners)
+template <int K>
+__device__ __forceinline__ void q_merges(uint32_t (&a)[kQPer], int t, int lane, uint32_t* xbuf, int& buf) {
+    if constexpr (K <= kQChunk) {
+        if constexpr (K <= 16) q_mirror_reg<K>(a);
+        else if constexpr (K <= 512) q_mirror_shfl<K>(a, lane);
+        else q_stage_smem<K / 16 - 1, true>(a, t, xbuf, buf);
+        q_cleaners<K / 4>(a, t, lane, xbuf, buf);
+        q_merges<2 * K>(a, t, lane, xbuf, buf);
+    }
+}
+
+// ------------------------------------------------------------------ SRAM-Quantiles pass
+// partial[blockIdx.x * 257 + j] = sum over this CTA's chunks c (c = blockIdx.x + k*gridDim.x)
+// of the chunk's j-th sample quantile (binary64).
+__global__ void __launch_bounds__(kQThreads) sram_quantiles_kernel(const float* __restrict__ x, int64_t n,
+                                                                    int64_t nchunks, double* __restrict__ partial) {
+    extern __shared__ __align__(16) uint32_t xbuf[];
+    const int t = threadIdx.x, lane = t & 31;
+    int buf = 0;
+    double acc = 0.0, acc256 = 0.0;  // quantile j = t; thread 0 also owns j = 256
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        const int64_t base = c * kQChunk;
+        const int64_t left = n - base;
+        const int m = left < kQChunk ? static_cast<int>(left) : kQChunk;
+        uint32_t a[kQPer];
+        // which element lands in which register does not matter (the network sorts the set):
+        // coalesced float4 loads, the chunk's tail padded with the largest key
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int e = 4 * (t + kQThreads * q);
+            if (e + 4 <= m) {
+                const float4 v = __ldcs(reinterpret_cast<const float4*>(x + base + e));
+                a[4 * q] = qkey(v.x);
+                a[4 * q + 1] = qkey(v.y);
+                a[4 * q + 2] = qkey(v.z);
+                a[4 * q + 3] = qkey(v.w);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; i++) a[4 * q + i] = (e + i < m) ? qkey(x[base + e + i]) : 0xffffffffu;
+            }
+        }
+        q_merges<2>(a, t, lane, xbuf, buf);
+        // sorted: key e = 16 t + r is a[r] of thread t; publish and read the order statistics
+        uint32_t* s = xbuf + buf * kQChunk;
+        buf ^= 1;
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+            *reinterpret_cast<uint4*>(s + qslot(t, q)) = make_uint4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+        __syncthreads();
+        {
+            const int i = static_cast<int>((static_cast<int64_t>(t) * m) / kQuantiles);  // Q2
+            acc += static_cast<double>(qval(s[qslot(i >> 4, (i >> 2) & 3) + (i & 3)]));
+        }
+        if (t == 0) {
+            const int i = static_cast<int>((256LL * m) / kQuantiles);
+            acc256 += static_cast<double>(qval(s[qslot(i >> 4, (i >> 2) & 3) + (i & 3)]));
+        }
+    }
+    partial[static_cast<int64_t>(blockIdx.x) * kQuantiles + t] = acc;
+    if (t == 0) partial[static_cast<int64_t>(blockIdx.x) * kQuantiles + 256] = acc256;
+}
+
+// ------------------------------------------------------------------ finalize (one CTA)
+// quantiles[j] = RN32( (sum_b partial[b][j]) / nchunks ) (Q4); if code != NULL also the Eq.5
+// quantile data type (Q5): mid_i = (Q_i + Q_{i+1}) * 0.5 in binary64, code_i = RN32(mid_i / max|mid|)
+// (all zeros when every midpoint is 0).
+__global__ void __launch_bounds__(512) quantiles_finalize_kernel(const double* __restrict__ partial, int nrows,
+                                                                 int64_t nchunks, float* __restrict__ quantiles,
+                                                                 float* __restrict__ code) {
+    __shared__ float q[kQuantiles];
+    __shared__ double wmax[16];
+    const int j = threadIdx.x;
+    if (j < kQuantiles) {
+        double s = 0.0;
+        for (int b = 0; b < nrows; b++) s += partial[static_cast<int64_t>(b) * kQuantiles + j];
+        const float v = static_cast<float>(s / static_cast<double>(nchunks));
+        q[j] = v;
+        quantiles[j] = v;
+    }
+    if (code == nullptr) return;
+    __syncthreads();
+    double mid = 0.0;
+    if (j < 256) mid = (static_cast<double>(q[j]) + static_cast<double>(q[j + 1])) * 0.5;
+    double m = fabs(mid);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((j & 31) == 0) wmax[j >> 5] = m;
+    __syncthreads();
+    double M = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); w++) M = fmax(M, wmax[w]);
+    if (j < 256) code[j] = M > 0.0 ? static_cast<float>(mid / M) : 0.0f;
+}
+
+}  // namespace q8

@@ -83,6 +83,9 @@ WORKLOADS = {
     # ratio per tensor), measured with the same bench contract
     "lamb_gpt2_xl": dict(kind="lamb", grad_dtype="bfloat16", shapes=gpt2_shapes(1600, 48), layerwise=True,
                          desc="8-bit LAMB, GPT-2-XL 580-tensor layer list, bf16 grads"),
+    # SURVEY 8(f) row 4 (App G): SRAM-Quantiles over a GPT-2-XL-sized fp32 buffer
+    "quantiles_gpt2_xl": dict(kind="adamw", grad_dtype="float32", shapes=gpt2_shapes(1600, 48), quantiles=True,
+                              desc="SRAM-Quantiles + Eq.5 codebook over a 1.5B fp32 GPT-2-XL-sized buffer"),
     "lars_resnet50": dict(kind="lars", grad_dtype="float16", shapes=resnet50_shapes(), layerwise=True,
                           desc="8-bit LARS, ResNet-50 161-tensor layer list, fp16 grads"),
 }

@@ -7,6 +7,7 @@ import re
 
 import numpy as np
 import pytest
+import torch
 
 import oracle
 import paper_2110_02861_b200 as q8
@@ -134,3 +135,25 @@ def test_layerwise_validation():
     rc = B.lib.q8_optim8bit_step(B.Q8_LAMB, FAKE, FAKE, B.Q8_BF16, FAKE, FAKE, FAKE, FAKE, 4096, 2048,
                                  ctypes.byref(_hp()), 1, None)
     assert rc == B.Q8_ERR_INVALID and "layer-wise" in B.lib.q8_last_error().decode()
+
+
+def test_quantile_validation_without_device():
+    # argument checks happen before any device work (include/q8.h)
+    assert B.lib.q8_estimate_quantiles(FAKE, 0, FAKE, None, FAKE, 1 << 20, None) == B.Q8_ERR_INVALID
+    assert B.lib.q8_estimate_quantiles(None, 10, FAKE, None, FAKE, 1 << 20, None) == B.Q8_ERR_INVALID
+    assert B.lib.q8_estimate_quantiles(FAKE + 4, 10, FAKE, None, FAKE, 1 << 20, None) == B.Q8_ERR_INVALID
+    assert B.lib.q8_create_quantile_codebook(None, None) == B.Q8_ERR_INVALID
+    z = np.zeros(257, np.float32)
+    out = np.zeros(256, np.float32)
+    assert B.lib.q8_create_quantile_codebook(z.ctypes.data, out.ctypes.data) == B.Q8_ERR_INVALID
+
+
+def test_host_quantile_codebook_matches_oracle():
+    # host function of the library vs the oracle (independent implementations of Eq.5 / Q5)
+
+    rng = np.random.default_rng(0)
+    for q in (np.sort(rng.standard_normal(257)).astype(np.float32),
+              np.sort(rng.exponential(size=257)).astype(np.float32) - np.float32(3.0),
+              np.linspace(0, 1, 257).astype(np.float32)):
+        lib_c = B.create_quantile_codebook(torch.from_numpy(q)).numpy()
+        np.testing.assert_array_equal(lib_c.view(np.uint32), oracle.quantile_codebook(q).view(np.uint32))

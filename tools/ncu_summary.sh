@@ -8,6 +8,6 @@ keep = {"Duration","DRAM Throughput","Memory Throughput","Compute (SM) Throughpu
 for row in csv.reader(sys.stdin):
     if len(row) < 12 or row[0] == "ID": continue
     name = row[-4] if False else None
-    metric, unit, val = row[-3], row[-2], row[-1]
+    metric, unit, val = row[12], row[13], row[14]
     if metric in keep: print(f"{row[4][:40]:40s} {metric:38s} {val:>16s} {unit}")
 '
