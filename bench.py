@@ -323,31 +323,69 @@ def main():
                 "frac_of_8TBs_spec": achieved / 8000.0, "kernel": "optim8bit_step_kernel",
                 "kernel_ms": kern_ms_max}
 
-    # ---- end to end through the public API with host buffers: per step the bf16 gradients
-    #      arrive from pinned host memory and the updated fp32 parameters go back to the host
-    e2e = None
+    # ---- end to end through the public API with HOST buffers (the C-ABI caller's view): every
+    #      buffer the step reads or writes lives in pinned host memory -- p, g, s1, s2, absmax1/2
+    #      go host -> device, the updated p, s1, s2, absmax1/2 come back, every step.  Pipelined over
+    #      chunks of whole blocks (blocks are independent, so a chunked step is bit-identical to
+    #      one call): H2D of chunk k+1 || step of chunk k || D2H of chunk k-1 on three streams, both
+    #      PCIe directions concurrently.  A second variant keeps the optimizer state resident in HBM
+    #      (a training loop's view): only the gradients come in and the parameters go out.
+    e2e = e2e_res = None
     if not args.no_e2e and args.e2e_steps > 0:
-        g_host = torch.empty(shard, dtype=TORCH_DT[gdt]).pin_memory()
-        g_host.copy_(gpool[0])
-        p_host = torch.empty(shard, dtype=torch.float32).pin_memory()
-        # Pipelined over chunks of whole blocks (blocks are independent, so a chunked step is
-        # bit-identical to one call): H2D of chunk k+1 || step of chunk k || D2H of chunk k-1, on
-        # three streams; both PCIe directions run concurrently.
         C = 1 << 25
         chunks = [(lo, min(lo + C, shard)) for lo in range(0, shard, C)]
+        nbs = (shard + 2047) // 2048
+        host = {"p": torch.empty(shard, dtype=torch.float32).pin_memory(),
+                "g": torch.empty(shard, dtype=TORCH_DT[gdt]).pin_memory(),
+                "s1": torch.empty(shard, dtype=torch.uint8).pin_memory(),
+                "s2": torch.empty(shard, dtype=torch.uint8).pin_memory(),
+                "a1": torch.empty(nbs, dtype=torch.float32).pin_memory(),
+                "a2": torch.empty(nbs, dtype=torch.float32).pin_memory()}
+        for k_, t_ in (("p", p), ("g", gpool[0]), ("s1", s1), ("s2", s2), ("a1", a1), ("a2", a2)):
+            host[k_].copy_(t_)
         s_in, s_cmp, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        gbuf = [torch.empty(C, dtype=TORCH_DT[gdt], device=dev) for _ in range(2)]
+        dbuf = [{k_: torch.empty(C if k_ not in ("a1", "a2") else C // 2048, dtype=v.dtype, device=dev)
+                 for k_, v in host.items()} for _ in range(2)]
         ev_in = [torch.cuda.Event() for _ in range(2)]
         ev_cmp = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
 
-        def one_e2e():
+        def one_e2e_host():
+            nonlocal step
+            step += 1
+            for k, (lo, hi) in enumerate(chunks):
+                b, m_, blo, bhi = k % 2, hi - lo, lo // 2048, (hi + 2047) // 2048
+                d = dbuf[b]
+                s_in.wait_event(ev_out[b])                  # chunk k-2's results have left this buffer
+                with torch.cuda.stream(s_in):
+                    for k_ in ("p", "g", "s1", "s2"):
+                        d[k_][:m_].copy_(host[k_][lo:hi], non_blocking=True)
+                    for k_ in ("a1", "a2"):
+                        d[k_][:bhi - blo].copy_(host[k_][blo:bhi], non_blocking=True)
+                ev_in[b].record(s_in)
+                s_cmp.wait_event(ev_in[b])
+                with torch.cuda.stream(s_cmp):
+                    q8.optim8bit_step(kind, d["p"][:m_], d["g"][:m_], d["s1"][:m_], d["s2"][:m_],
+                                      d["a1"][:bhi - blo], d["a2"][:bhi - blo], step=step, hp=hpo, lr=hp["lr"])
+                ev_cmp[b].record(s_cmp)
+                s_out.wait_event(ev_cmp[b])
+                with torch.cuda.stream(s_out):
+                    for k_ in ("p", "s1", "s2"):
+                        host[k_][lo:hi].copy_(d[k_][:m_], non_blocking=True)
+                    for k_ in ("a1", "a2"):
+                        host[k_][blo:bhi].copy_(d[k_][:bhi - blo], non_blocking=True)
+                ev_out[b].record(s_out)
+
+        gbuf = [torch.empty(C, dtype=TORCH_DT[gdt], device=dev) for _ in range(2)]
+
+        def one_e2e_resident():
             nonlocal step
             step += 1
             for k, (lo, hi) in enumerate(chunks):
                 b = k % 2
                 s_in.wait_event(ev_cmp[b])                  # chunk k-2 has consumed this buffer
                 with torch.cuda.stream(s_in):
-                    gbuf[b][:hi - lo].copy_(g_host[lo:hi], non_blocking=True)
+                    gbuf[b][:hi - lo].copy_(host["g"][lo:hi], non_blocking=True)
                 ev_in[b].record(s_in)
                 s_cmp.wait_event(ev_in[b])
                 with torch.cuda.stream(s_cmp):
@@ -357,30 +395,41 @@ def main():
                 ev_cmp[b].record(s_cmp)
                 s_out.wait_event(ev_cmp[b])
                 with torch.cuda.stream(s_out):
-                    p_host[lo:hi].copy_(p[lo:hi], non_blocking=True)
+                    host["p"][lo:hi].copy_(p[lo:hi], non_blocking=True)
 
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        cur = torch.cuda.current_stream(dev)
-        a.record(cur)
-        for st_ in (s_in, s_cmp, s_out):
-            st_.wait_stream(cur)
-        for _ in range(args.e2e_steps):
-            one_e2e()
-        for st_ in (s_in, s_cmp, s_out):
-            cur.wait_stream(st_)
-        b.record(cur)
-        torch.cuda.synchronize()
-        em = torch.tensor([a.elapsed_time(b) / args.e2e_steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(em, op=dist.ReduceOp.MAX)
-        e2e = {"value": n_total / (float(em[0]) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": n_pad * g_host.element_size(), "d2h_bytes_per_step": n_pad * 4,
-               "ms_per_step": float(em[0]), "chunks_per_step": len(chunks),
-               "path": "pinned host bf16 grads -> H2D || q8_optim8bit_step || D2H fp32 params, pipelined over "
-                       "32M-param chunks on three streams"}
+        def timed(fn):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            cur = torch.cuda.current_stream(dev)
+            a.record(cur)
+            for st_ in (s_in, s_cmp, s_out):
+                st_.wait_stream(cur)
+            for _ in range(args.e2e_steps):
+                fn()
+            for st_ in (s_in, s_cmp, s_out):
+                cur.wait_stream(st_)
+            b.record(cur)
+            torch.cuda.synchronize()
+            em = torch.tensor([a.elapsed_time(b) / args.e2e_steps], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(em, op=dist.ReduceOp.MAX)
+            return float(em[0])
+
+        ms_h = timed(one_e2e_host)
+        e2e = {"value": n_total / (ms_h / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": shard * (4 + host["g"].element_size() + 2) + nbs * 8,
+               "d2h_bytes_per_step": shard * (4 + 2) + nbs * 8, "ms_per_step": ms_h, "chunks_per_step": len(chunks),
+               "path": "all step buffers in pinned host memory: H2D p, g, s1, s2, absmax1/2 || q8_optim8bit_step || "
+                       "D2H p, s1, s2, absmax1/2, pipelined over 32M-param chunks on three streams"}
+        ms_r = timed(one_e2e_resident)
+        e2e_res = {"value": n_total / (ms_r / 1e3), "unit": UNIT,
+                   "h2d_bytes_per_step": shard * host["g"].element_size(), "d2h_bytes_per_step": shard * 4,
+                   "ms_per_step": ms_r, "chunks_per_step": len(chunks),
+                   "path": "optimizer state resident in HBM: pinned host grads -> H2D || q8_optim8bit_step || "
+                           "D2H fp32 params, pipelined over 32M-param chunks on three streams"}
+        del host, dbuf, gbuf
 
     # ---- ZeRO-1 round trip (N > 1): reduce-scatter bf16 grads -> shard step -> all-gather params
     zero1 = None
@@ -450,7 +499,8 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic: p~N(0,0.02^2), bf16 g~N(0,1e-3^2) (pool of 2), 8-bit states evolved from zero "
                     f"over the warm-up; most common s1 code after warm-up holds {100 * share1:.1f}% of elements",
-            "config": cfg, "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e, "zero1": zero1,
+            "config": cfg, "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
+            "e2e_resident_states": e2e_res, "zero1": zero1,
             "gpu_launches": args.steps, "clocks": clk.summary(),
             "achieved_gbs_whole_job": n_total * bpp / (ms_per_step / 1e3) / 1e9,
             "library": q8.version(),
