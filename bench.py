@@ -246,6 +246,8 @@ def main():
     cfg = workload_config(args.workload, world)
     if synth.WORKLOADS[args.workload].get("layerwise"):
         return main_layerwise(args, cfg, q8, world, rank, local, dev)
+    if synth.WORKLOADS[args.workload].get("multi"):
+        return main_multi(args, cfg, q8, world, rank, local, dev)
     if synth.WORKLOADS[args.workload].get("quantiles"):
         return main_quantiles(args, cfg, q8, world, rank, local, dev)
     kind, gdt = cfg["kind"], cfg["grad_dtype"]
@@ -614,6 +616,128 @@ def main_layerwise(args, cfg, q8, world, rank, local, dev):
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
                          else "fallback 6.65 TB/s (B200_PROFILING.md)"},
             "cpu_baseline": cpu_baseline, "e2e": None, "gpu_launches": args.steps * 3 * chunks,
+            "clocks": clk.summary(), "library": q8.version(),
+        }))
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+def main_multi(args, cfg, q8, world, rank, local, dev):
+    """Multi-tensor workloads (BASELINE config 3: 8-bit Momentum over ResNet-50's 161 tensors, 99 of
+    them smaller than one block): per-tensor blocks, the tensors are views of one flat
+    allocation at 16-element aligned offsets.  A step is ONE q8_optim8bit_step_multi launch (a9);
+    the same step as 161 single-tensor q8_optim8bit_step launches is timed beside it.  N > 1 runs
+    independent replicas (weak scaling)."""
+    kind, gdt = cfg["kind"], cfg["grad_dtype"]
+    hp = dict(cfg["hparams"])
+    sizes = [synth.numel(s) for s in synth.WORKLOADS[args.workload]["shapes"]]
+    offs, o = [], 0
+    for n in sizes:
+        offs.append(o)
+        o += (n + 15) // 16 * 16
+    total = o
+    two = kind not in ("momentum", "lars")
+    p = synth.params(total, seed=1 + rank, device=dev)
+    gpool = [synth.grads(total, step=t, seed=rank, dtype=gdt, device=dev) for t in (1, 2)]
+    nbt = sum((n + 2047) // 2048 for n in sizes)
+    s1 = torch.zeros(total, dtype=torch.uint8, device=dev)
+    s2 = torch.zeros(total if two else 0, dtype=torch.uint8, device=dev)
+    a1 = torch.zeros(nbt, dtype=torch.float32, device=dev)
+    a2 = torch.zeros(nbt if two else 0, dtype=torch.float32, device=dev)
+
+    def entries(g):
+        ents, bo = [], 0
+        for n, off in zip(sizes, offs):
+            nb = (n + 2047) // 2048
+            ents.append((p[off:off + n], g[off:off + n], s1[off:off + n], s2[off:off + n] if two else None,
+                         a1[bo:bo + nb], a2[bo:bo + nb] if two else None))
+            bo += nb
+        return ents
+
+    ents = [entries(g) for g in gpool]
+    tls = [q8.TensorList(e) for e in ents]
+    hpo = q8.hparams(**hp)
+    step = 0
+
+    def one_multi(i):
+        nonlocal step
+        step += 1
+        q8.optim8bit_step_multi(kind, tls[i % 2], lr=hp["lr"], step=step, hp=hpo)
+
+    def one_single(i):
+        nonlocal step
+        step += 1
+        for (pt, gt, c1, c2, b1, b2) in ents[i % 2]:
+            q8.optim8bit_step(kind, pt, gt, c1, c2, b1, b2, step=step, hp=hpo, lr=hp["lr"])
+
+    # inputs of one step are ~0.3 GB, close to the 126 MB L2: flush with a 256 MB write between
+    # steps, outside the timed events
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, steps):
+        for i in range(args.warmup):
+            fn(i)
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(steps):
+            flush.fill_(i & 0xff)
+            ev[i][0].record(stream)
+            fn(i)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        ms = torch.tensor([statistics.mean(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms[0])
+
+    with ClockSampler(local) as clk:
+        ms_multi = timed(one_multi, args.steps)
+    ms_single = timed(one_single, max(3, args.steps // 4))
+    n_total = sum(sizes)
+    bpp = bytes_per_param(kind, gdt)
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = n_total * bpp / (ms_multi / 1e3) / 1e9
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        pc = p.cpu().numpy().copy()
+        gc = synth.to_f32_numpy(gpool[0])
+        s1c, a1c = s1.cpu().numpy().copy(), a1.cpu().numpy().copy()
+        s2c = s2.cpu().numpy().copy() if two else None
+        a2c = a2.cpu().numpy().copy() if two else None
+        t0, bo = time.perf_counter(), 0
+        for n, off in zip(sizes, offs):
+            nb = (n + 2047) // 2048
+            oracle.optim8bit_step(kind, pc[off:off + n], gc[off:off + n], s1c[off:off + n],
+                                  s2c[off:off + n] if two else None, a1c[bo:bo + nb],
+                                  a2c[bo:bo + nb] if two else None, step=3, **hp)
+            bo += nb
+        dt = time.perf_counter() - t0
+        cpu_baseline = {"value": n_total / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+                        "sample": f"the whole {len(sizes)}-tensor list, one {kind} step, 1 thread, {dt:.1f} s"}
+    if rank == 0:
+        cfg = dict(cfg, parallelism=f"replicas-{world}" if world > 1 else "single-gpu", tensors=len(sizes),
+                   tensors_below_one_block=sum(1 for n in sizes if n < 2048),
+                   l2="flush 256 MB between steps (outside the timed events)")
+        print(json.dumps({
+            "metric": METRIC, "value": world * n_total / (ms_multi / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_multi, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": f"synthetic: p~N(0,0.02^2), {gdt} g~N(0,1e-3^2) (pool of 2), states evolved from zero",
+            "config": cfg,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "bytes_per_param": bpp, "algorithmic_bytes_per_launch": n_total * bpp,
+                         "kernel": "optim8bit_step_kernel (multi-tensor, one launch)",
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
+                         else "fallback 6.65 TB/s (B200_PROFILING.md)"},
+            "single_tensor_launches": {"ms_per_step": ms_single, "launches_per_step": len(sizes),
+                                       "value": n_total / (ms_single / 1e3)},
+            "cpu_baseline": cpu_baseline, "e2e": None, "gpu_launches": args.steps,
             "clocks": clk.summary(), "library": q8.version(),
         }))
     if dist.is_initialized():

@@ -73,7 +73,7 @@ WORKLOADS = {
                     desc="codec round-trip + 10 steps 8-bit Adam, one flat 1M fp32 tensor"),
     "cfg2_gpt2_medium": dict(kind="adam", grad_dtype="float16", shapes=gpt2_shapes(1024, 24),
                              desc="8-bit Adam, 355M GPT-2-medium flat buffer, fp16 grads"),
-    "cfg3_resnet50": dict(kind="momentum", grad_dtype="float16", shapes=resnet50_shapes(),
+    "cfg3_resnet50": dict(kind="momentum", grad_dtype="float16", shapes=resnet50_shapes(), multi=True,
                           desc="8-bit Momentum, ResNet-50 tensor list, multi-tensor launch"),
     "cfg4_gpt2_xl": dict(kind="adamw", grad_dtype="bfloat16", shapes=gpt2_shapes(1600, 48),
                          desc="8-bit AdamW, 1.5B GPT-2-XL flat buffer, bf16 grads"),
