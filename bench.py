@@ -177,7 +177,19 @@ def oracle_sample(cfg, target_s: float = 10.0):
     n2 = max(2048, n2 // 2048 * 2048)
     dt2, _ = run(n2)
     return n2 / dt2, cores, (f"{n2:,} parameters ({n2 // 2048:,} whole blocks) of {cfg['workload'].split(':')[0]}, "
-                             f"one {kind} step, {cores} threads, {dt2:.1f} s")
+                             f"one {kind} step, {cores} threads, {dt2:.1f} s, {cpu_model()}, "
+                             f"{1e9 * dt2 / n2:.2f} ns/param")
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "cpu model unknown"
 
 
 def run_reference(args):
@@ -465,7 +477,8 @@ def main():
         zero1 = {"ms_per_step": tot, "params_per_s": n_total / (tot / 1e3), "reduce_scatter_ms": float(zt[0]),
                  "shard_step_ms": float(zt[1]), "all_gather_ms": float(zt[2]),
                  "reduce_scatter_bytes_per_rank": n_pad * (2 if gdt != "float32" else 4),
-                 "all_gather_bytes_per_rank": n_pad * 4, "backend": "nccl", "steps": args.zero1_steps}
+                 "all_gather_bytes_per_rank": n_pad * 4, "backend": "nccl", "steps": args.zero1_steps,
+                 "check": zero1_check(zo, q8, kind, hp)}
         del zo
         torch.cuda.empty_cache()
         if args.zero_fused:
@@ -510,6 +523,35 @@ def main():
         print(json.dumps(out))
     if dist.is_initialized():
         dist.destroy_process_group()
+
+
+def zero1_check(zo, q8, kind, hp):
+    """SURVEY 8(e) correctness: one more ZeRO-1 step, compared with the unsharded step on the same
+    REDUCED gradient (NCCL's reduction order differs from any local sum): the reduced shards and
+    the initial states are all-gathered, every rank runs the 1-GPU step on the full buffer and
+    compares parameters, codes and absmax bit for bit; the verdict is agreed by all ranks."""
+    def gather(t):
+        out = torch.empty(t.numel() * zo.world, dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, t.contiguous())
+        return out
+
+    p_ref = zo.params.clone()
+    st = [gather(t) if t is not None else None for t in (zo.s1, zo.s2, zo.absmax1, zo.absmax2)]
+    zo.grads[:zo.n].normal_(0, 1e-3)
+    zo.reduce_scatter()
+    g_full = gather(zo.g_shard)
+    zo.shard_step()
+    zo.all_gather()
+    q8.optim8bit_step(kind, p_ref, g_full, st[0], st[1], st[2], st[3], step=zo.t, lr=hp["lr"],
+                      **{k: v for k, v in hp.items() if k != "lr"})
+    new = [gather(t) if t is not None else None for t in (zo.s1, zo.s2, zo.absmax1, zo.absmax2)]
+    ok = torch.equal(zo.params.view(torch.int32), p_ref.view(torch.int32))
+    for a, b in zip(new, st):
+        if a is not None:
+            ok = ok and torch.equal(a.view(torch.uint8), b.view(torch.uint8))
+    flag = torch.tensor([0 if ok else 1], dtype=torch.int32, device=zo.params.device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+    return "bit-exact vs the unsharded step on the reduced gradient" if int(flag[0]) == 0 else "MISMATCH"
 
 
 def main_layerwise(args, cfg, q8, world, rank, local, dev):
