@@ -10,7 +10,8 @@
 //     per-stage direction logic.  Comparators whose partners live in the same thread are
 //     register min/max; partners in the same warp are exchanged with SHFL (j = 16..256); only
 //     the 6 stages with partners in another warp (j >= 512) go through shared memory, double-
-//     buffered so each needs one barrier.  Keys are the monotone unsigned image of the fp32 bits.
+//     buffered so each needs one barrier.  Keys are the fp32 values (FMNMX); cross-thread
+//     comparators run in signed views so that they too cost one FMNMX per key (see below).
 //   * the 257 order statistics floor(j*m/257) (Q1, Q2) are read from the sorted chunk and summed
 //     per thread in binary64 registers across the CTA's chunks (Q4); one partial row per CTA.
 //   * a one-CTA finalize kernel sums the partial rows in CTA order, divides by the chunk count,
@@ -28,167 +29,208 @@ constexpr int kQPer = kQChunk / kQThreads;  // 16 keys per thread
 constexpr int kQuantiles = 257;        // Q_X(j/257), j = 0..256 (Eq.5, reading Q1)
 constexpr int kQSmemBytes = 2 * kQChunk * 4;  // two 16 KB exchange buffers
 
-// monotone unsigned key of an fp32 value (total order, -0 < +0) and back
-__device__ __forceinline__ uint32_t qkey(float f) {
-    const uint32_t b = __float_as_uint(f);
-    return b ^ (static_cast<uint32_t>(static_cast<int32_t>(b) >> 31) | 0x80000000u);
-}
-__device__ __forceinline__ float qval(uint32_t k) {
-    return __uint_as_float(k ^ ((k >> 31) ? 0x80000000u : 0xffffffffu));
-}
+// Keys are the fp32 values themselves (zeros canonicalized to +0 on load: -0 and +0 are equal
+// values, reading Q2 compares values), compared with FMNMX.  In-thread comparators have
+// compile-time roles (one FMNMX per key).  For comparators whose partner is another thread, the
+// lower thread keeps the min and the upper the max; to make that ONE instruction on both sides each
+// thread holds its keys in a signed "view" v = s*key during such stages (s = +1 lower, -1 upper):
+// then both compute v = min(v, -v_partner) (the negation is an FMNMX operand modifier), since for
+// the upper thread -min(-a, -b) = max(a, b).  Changing views is an exact multiply by +-1 on the FMA
+// pipe, which this kernel otherwise leaves idle.
 
 // word offset of key e = 16 t + r in an exchange buffer: thread t's four quads are permuted by
 // (t >> 1) & 3 so eight consecutive threads' 16-byte accesses hit eight distinct bank groups
 __device__ __forceinline__ int qslot(int t, int q) { return 16 * t + 4 * (q ^ ((t >> 1) & 3)); }
 
+__device__ __forceinline__ void q_scale(float (&a)[kQPer], float f) {
+#pragma unroll
+    for (int r = 0; r < kQPer; r++) a[r] = __fmul_rn(a[r], f);  // f = +-1: exact
+}
+
 // ------------------------------------------------------------------ comparator stages
-// in-thread half-cleaner, distance J in {1, 2, 4, 8}
+// in-thread half-cleaner, distance J in {1, 2, 4, 8} (key space)
 template <int J>
-__device__ __forceinline__ void q_ce_reg(uint32_t (&a)[kQPer]) {
+__device__ __forceinline__ void q_ce_reg(float (&a)[kQPer]) {
 #pragma unroll
     for (int r = 0; r < kQPer; r++)
         if (!(r & J)) {
-            const uint32_t x = a[r], y = a[r | J];
-            a[r] = min(x, y);
-            a[r | J] = max(x, y);
+            const float x = a[r], y = a[r | J];
+            a[r] = fminf(x, y);
+            a[r | J] = fmaxf(x, y);
         }
 }
 
-// in-thread mirror stage of merge size K in {2, 4, 8, 16}: r <-> r ^ (K-1)
+// in-thread mirror stage of merge size K in {2, 4, 8, 16}: r <-> r ^ (K-1) (key space)
 template <int K>
-__device__ __forceinline__ void q_mirror_reg(uint32_t (&a)[kQPer]) {
+__device__ __forceinline__ void q_mirror_reg(float (&a)[kQPer]) {
 #pragma unroll
     for (int r = 0; r < kQPer; r++)
         if (!(r & (K / 2))) {
             const int p = r ^ (K - 1);
-            const uint32_t x = a[r], y = a[p];
-            a[r] = min(x, y);
-            a[p] = max(x, y);
+            const float x = a[r], y = a[p];
+            a[r] = fminf(x, y);
+            a[p] = fmaxf(x, y);
         }
 }
 
-// warp half-cleaner: partner lane ^ M (M in 1..16), same register; the lower thread keeps min
+// enter the view of a cross-thread stage whose upper side is `upper` (s_cur: the current view)
+__device__ __forceinline__ void q_enter(float (&a)[kQPer], float& s_cur, bool upper) {
+    const float s_new = upper ? -1.0f : 1.0f;
+    q_scale(a, s_cur * s_new);
+    s_cur = s_new;
+}
+
+// warp half-cleaner: partner lane ^ M (M in 1..16), same register
 template <int M>
-__device__ __forceinline__ void q_ce_shfl(uint32_t (&a)[kQPer], int lane) {
-    const bool lower = !(lane & M);
+__device__ __forceinline__ void q_ce_shfl(float (&a)[kQPer], int lane, float& s_cur) {
+    q_enter(a, s_cur, lane & M);
 #pragma unroll
-    for (int r = 0; r < kQPer; r++) {
-        const uint32_t o = __shfl_xor_sync(0xffffffffu, a[r], M);
-        a[r] = lower ? min(a[r], o) : max(a[r], o);
-    }
+    for (int r = 0; r < kQPer; r++) a[r] = fminf(a[r], -__shfl_xor_sync(0xffffffffu, a[r], M));
 }
 
 // warp mirror stage of merge size K in {32..512}: partner lane ^ (K/16 - 1), register 15 - r
 template <int K>
-__device__ __forceinline__ void q_mirror_shfl(uint32_t (&a)[kQPer], int lane) {
+__device__ __forceinline__ void q_mirror_shfl(float (&a)[kQPer], int lane, float& s_cur) {
     constexpr int M = K / 16 - 1;
-    const bool lower = !(lane & (K / 32));
-    uint32_t o[kQPer];
+    q_enter(a, s_cur, lane & (K / 32));
+    float o[kQPer];
 #pragma unroll
     for (int r = 0; r < kQPer; r++) o[r] = __shfl_xor_sync(0xffffffffu, a[kQPer - 1 - r], M);
 #pragma unroll
-    for (int r = 0; r < kQPer; r++) a[r] = lower ? min(a[r], o[r]) : max(a[r], o[r]);
+    for (int r = 0; r < kQPer; r++) a[r] = fminf(a[r], -o[r]);
 }
 
 // cross-warp stage through shared memory: partner thread t ^ T; MIRROR reverses the registers
-// (mirror of merge size K: T = K/16 - 1, lower bit K/32).  `buf` alternates between the two
+// (mirror of merge size K: T = K/16 - 1, upper bit K/32).  `buf` alternates between the two
 // exchange buffers, so one barrier per stage suffices (a buffer is rewritten only after the
 // next stage's barrier, which every thread reaches after its reads of this one).
 template <int T, bool MIRROR>
-__device__ __forceinline__ void q_stage_smem(uint32_t (&a)[kQPer], int t, uint32_t* xbuf, int& buf) {
-    uint32_t* s = xbuf + buf * kQChunk;
+__device__ __forceinline__ void q_stage_smem(float (&a)[kQPer], int t, float* xbuf, int& buf, float& s_cur) {
+    q_enter(a, s_cur, MIRROR ? (t & ((T + 1) / 2)) : (t & T));
+    float* s = xbuf + buf * kQChunk;
     buf ^= 1;
 #pragma unroll
     for (int q = 0; q < 4; q++)
-        *reinterpret_cast<uint4*>(s + qslot(t, q)) = make_uint4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+        *reinterpret_cast<float4*>(s + qslot(t, q)) = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
     __syncthreads();
     const int pt = t ^ T;
-    const bool lower = MIRROR ? !(t & ((T + 1) / 2)) : !(t & T);
-    uint32_t o[kQPer];
+    float o[kQPer];
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-        const uint4 v = *reinterpret_cast<const uint4*>(s + qslot(pt, q));
+        const float4 v = *reinterpret_cast<const float4*>(s + qslot(pt, q));
         o[4 * q] = v.x;
         o[4 * q + 1] = v.y;
         o[4 * q + 2] = v.z;
         o[4 * q + 3] = v.w;
     }
 #pragma unroll
-    for (int r = 0; r < kQPer; r++) {
-        const uint32_t p = MIRROR ? o[kQPer - 1 - r] : o[r];
-        a[r] = lower ? min(a[r], p) : max(a[r], p);
+    for (int r = 0; r < kQPer; r++) a[r] = fminf(a[r], -(MIRROR ? o[kQPer - 1 - r] : o[r]));
+}
+
+// Per-thread context of the network: the two block-wide exchange buffers (cross-warp stages).
+struct QCtx {
+    int t, lane;
+    float* xbuf;   // 2 x 4096 words
+    int buf;
+};
+
+// in-register half-cleaners J, J/2, ..., 1 (key space)
+template <int J>
+__device__ __forceinline__ void q_cleaners_reg(float (&a)[kQPer]) {
+    if constexpr (J >= 1) {
+        q_ce_reg<J>(a);
+        q_cleaners_reg<J / 2>(a);
     }
 }
 
-// half-cleaners of distance J, J/2, ..., 1 (key e = 16 t + r: J < 16 in registers, J < 512
-// within the warp, else shared memory)
+// half-cleaners of distance J, J/2, ..., 1 in layout L0 (key e = 16 t + r: J < 16 in registers,
+// J < 512 within the warp, else shared memory).  Cross-thread stages run in views; the view is
+// left (back to key space) before the first in-register stage.
 template <int J>
-__device__ __forceinline__ void q_cleaners(uint32_t (&a)[kQPer], int t, int lane, uint32_t* xbuf, int& buf) {
+__device__ __forceinline__ void q_cleaners(float (&a)[kQPer], QCtx& c, float& s_cur) {
     if constexpr (J >= 1) {
-        if constexpr (J < 16) q_ce_reg<J>(a);
-        else if constexpr (J < 512) q_ce_shfl<J / 16>(a, lane);
-        else q_stage_smem<J / 16, false>(a, t, xbuf, buf);
-        q_cleaners<J / 2>(a, t, lane, xbuf, buf);
+        if constexpr (J < 16) {
+            q_scale(a, s_cur);
+            s_cur = 1.0f;
+            q_cleaners_reg<J>(a);
+        } else {
+            if constexpr (J < 512) q_ce_shfl<J / 16>(a, c.lane, s_cur);
+            else q_stage_smem<J / 16, false>(a, c.t, c.xbuf, c.buf, s_cur);
+            q_cleaners<J / 2>(a, c, s_cur);
+        }
     }
 }
 
 // bitonic merges of size K, 2K, ..., 4096 (flip form: mirror stage, then half-cleaners)
 template <int K>
-__device__ __forceinline__ void q_merges(uint32_t (&a)[kQPer], int t, int lane, uint32_t* xbuf, int& buf) {
+__device__ __forceinline__ void q_merges(float (&a)[kQPer], QCtx& c) {
     if constexpr (K <= kQChunk) {
+        float s_cur = 1.0f;
         if constexpr (K <= 16) q_mirror_reg<K>(a);
-        else if constexpr (K <= 512) q_mirror_shfl<K>(a, lane);
-        else q_stage_smem<K / 16 - 1, true>(a, t, xbuf, buf);
-        q_cleaners<K / 4>(a, t, lane, xbuf, buf);
-        q_merges<2 * K>(a, t, lane, xbuf, buf);
+        else if constexpr (K <= 512) q_mirror_shfl<K>(a, c.lane, s_cur);
+        else q_stage_smem<K / 16 - 1, true>(a, c.t, c.xbuf, c.buf, s_cur);
+        q_cleaners<K / 4>(a, c, s_cur);
+        q_merges<2 * K>(a, c);
     }
 }
 
 // ------------------------------------------------------------------ SRAM-Quantiles pass
 // partial[blockIdx.x * 257 + j] = sum over this CTA's chunks c (c = blockIdx.x + k*gridDim.x)
 // of the chunk's j-th sample quantile (binary64).
-__global__ void __launch_bounds__(kQThreads) sram_quantiles_kernel(const float* __restrict__ x, int64_t n,
+// 4 resident CTAs per SM (64 registers, no spills): the network's pipes (ALU for FMNMX, the
+// shared-memory crossbar for SHFL and the exchanges) are co-limits at ~60-70 % each, so more
+// warps to hide the SHFL / LDS latency is what pays (measured: 2 CTAs 11.4 ms, 3: 11.0, 4: 10.5).
+#ifndef Q8_QT_MINB
+#define Q8_QT_MINB 4
+#endif
+__global__ void __launch_bounds__(kQThreads, Q8_QT_MINB) sram_quantiles_kernel(const float* __restrict__ x, int64_t n,
                                                                     int64_t nchunks, double* __restrict__ partial) {
-    extern __shared__ __align__(16) uint32_t xbuf[];
+    extern __shared__ __align__(16) float xbuf[];
     const int t = threadIdx.x, lane = t & 31;
-    int buf = 0;
+    QCtx ctx;
+    ctx.t = t;
+    ctx.lane = lane;
+    ctx.xbuf = xbuf;
+    ctx.buf = 0;
     double acc = 0.0, acc256 = 0.0;  // quantile j = t; thread 0 also owns j = 256
     for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
         const int64_t base = c * kQChunk;
         const int64_t left = n - base;
         const int m = left < kQChunk ? static_cast<int>(left) : kQChunk;
-        uint32_t a[kQPer];
+        float a[kQPer];
         // which element lands in which register does not matter (the network sorts the set):
-        // coalesced float4 loads, the chunk's tail padded with the largest key
+        // coalesced float4 loads, zeros canonicalized (-0 + 0 = +0), the chunk's tail padded
+        // with +inf (never selected: every selected index is < m)
 #pragma unroll
         for (int q = 0; q < 4; q++) {
             const int e = 4 * (t + kQThreads * q);
             if (e + 4 <= m) {
                 const float4 v = __ldcs(reinterpret_cast<const float4*>(x + base + e));
-                a[4 * q] = qkey(v.x);
-                a[4 * q + 1] = qkey(v.y);
-                a[4 * q + 2] = qkey(v.z);
-                a[4 * q + 3] = qkey(v.w);
+                a[4 * q] = __fadd_rn(v.x, 0.0f);
+                a[4 * q + 1] = __fadd_rn(v.y, 0.0f);
+                a[4 * q + 2] = __fadd_rn(v.z, 0.0f);
+                a[4 * q + 3] = __fadd_rn(v.w, 0.0f);
             } else {
 #pragma unroll
-                for (int i = 0; i < 4; i++) a[4 * q + i] = (e + i < m) ? qkey(x[base + e + i]) : 0xffffffffu;
+                for (int i = 0; i < 4; i++)
+                    a[4 * q + i] = (e + i < m) ? __fadd_rn(x[base + e + i], 0.0f) : __int_as_float(0x7f800000);
             }
         }
-        q_merges<2>(a, t, lane, xbuf, buf);
+        q_merges<2>(a, ctx);
         // sorted: key e = 16 t + r is a[r] of thread t; publish and read the order statistics
-        uint32_t* s = xbuf + buf * kQChunk;
-        buf ^= 1;
+        float* s = xbuf + ctx.buf * kQChunk;
+        ctx.buf ^= 1;
 #pragma unroll
         for (int q = 0; q < 4; q++)
-            *reinterpret_cast<uint4*>(s + qslot(t, q)) = make_uint4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+            *reinterpret_cast<float4*>(s + qslot(t, q)) = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
         __syncthreads();
         {
             const int i = static_cast<int>((static_cast<int64_t>(t) * m) / kQuantiles);  // Q2
-            acc += static_cast<double>(qval(s[qslot(i >> 4, (i >> 2) & 3) + (i & 3)]));
+            acc += static_cast<double>(s[qslot(i >> 4, (i >> 2) & 3) + (i & 3)]);
         }
         if (t == 0) {
             const int i = static_cast<int>((256LL * m) / kQuantiles);
-            acc256 += static_cast<double>(qval(s[qslot(i >> 4, (i >> 2) & 3) + (i & 3)]));
+            acc256 += static_cast<double>(s[qslot(i >> 4, (i >> 2) & 3) + (i & 3)]);
         }
     }
     partial[static_cast<int64_t>(blockIdx.x) * kQuantiles + t] = acc;
