@@ -24,8 +24,13 @@
 namespace q8 {
 
 constexpr int kQChunk = 4096;          // "about 4096 32-bit values", reading Q3
-constexpr int kQThreads = 256;
-constexpr int kQPer = kQChunk / kQThreads;  // 16 keys per thread
+#ifndef Q8_QT_PER
+#define Q8_QT_PER 16
+#endif
+constexpr int kQPer = Q8_QT_PER;       // keys per thread (16 or 32)
+constexpr int kQThreads = kQChunk / kQPer;
+constexpr int kQQuads = kQPer / 4;
+static_assert(kQPer == 16 || kQPer == 32, "16 or 32 keys per thread");
 constexpr int kQuantiles = 257;        // Q_X(j/257), j = 0..256 (Eq.5, reading Q1)
 constexpr int kQSmemBytes = 2 * kQChunk * 4;  // two 16 KB exchange buffers
 
@@ -38,9 +43,11 @@ constexpr int kQSmemBytes = 2 * kQChunk * 4;  // two 16 KB exchange buffers
 // the upper thread -min(-a, -b) = max(a, b).  Changing views is an exact multiply by +-1 on the FMA
 // pipe, which this kernel otherwise leaves idle.
 
-// word offset of key e = 16 t + r in an exchange buffer: thread t's four quads are permuted by
-// (t >> 1) & 3 so eight consecutive threads' 16-byte accesses hit eight distinct bank groups
-__device__ __forceinline__ int qslot(int t, int q) { return 16 * t + 4 * (q ^ ((t >> 1) & 3)); }
+// word offset of key e = P t + r in an exchange buffer (P = kQPer): thread t's quads are permuted
+// so that eight consecutive threads' 16-byte accesses of one quad hit eight distinct bank groups
+__device__ __forceinline__ int qslot(int t, int q) {
+    return kQPer * t + 4 * (q ^ (kQPer == 16 ? ((t >> 1) & 3) : (t & 7)));
+}
 
 __device__ __forceinline__ void q_scale(float (&a)[kQPer], float f) {
 #pragma unroll
@@ -48,7 +55,7 @@ __device__ __forceinline__ void q_scale(float (&a)[kQPer], float f) {
 }
 
 // ------------------------------------------------------------------ comparator stages
-// in-thread half-cleaner, distance J in {1, 2, 4, 8} (key space)
+// in-thread half-cleaner, distance J < P (key space)
 template <int J>
 __device__ __forceinline__ void q_ce_reg(float (&a)[kQPer]) {
 #pragma unroll
@@ -60,7 +67,7 @@ __device__ __forceinline__ void q_ce_reg(float (&a)[kQPer]) {
         }
 }
 
-// in-thread mirror stage of merge size K in {2, 4, 8, 16}: r <-> r ^ (K-1) (key space)
+// in-thread mirror stage of merge size K <= P: r <-> r ^ (K-1) (key space)
 template <int K>
 __device__ __forceinline__ void q_mirror_reg(float (&a)[kQPer]) {
 #pragma unroll
@@ -80,7 +87,7 @@ __device__ __forceinline__ void q_enter(float (&a)[kQPer], float& s_cur, bool up
     s_cur = s_new;
 }
 
-// warp half-cleaner: partner lane ^ M (M in 1..16), same register
+// warp half-cleaner: partner lane ^ M (M in 1..16), same register (distance M*P)
 template <int M>
 __device__ __forceinline__ void q_ce_shfl(float (&a)[kQPer], int lane, float& s_cur) {
     q_enter(a, s_cur, lane & M);
@@ -88,11 +95,11 @@ __device__ __forceinline__ void q_ce_shfl(float (&a)[kQPer], int lane, float& s_
     for (int r = 0; r < kQPer; r++) a[r] = fminf(a[r], -__shfl_xor_sync(0xffffffffu, a[r], M));
 }
 
-// warp mirror stage of merge size K in {32..512}: partner lane ^ (K/16 - 1), register 15 - r
+// warp mirror stage of merge size K in (P, 32P]: partner lane ^ (K/P - 1), register P-1-r
 template <int K>
 __device__ __forceinline__ void q_mirror_shfl(float (&a)[kQPer], int lane, float& s_cur) {
-    constexpr int M = K / 16 - 1;
-    q_enter(a, s_cur, lane & (K / 32));
+    constexpr int M = K / kQPer - 1;
+    q_enter(a, s_cur, lane & (K / (2 * kQPer)));
     float o[kQPer];
 #pragma unroll
     for (int r = 0; r < kQPer; r++) o[r] = __shfl_xor_sync(0xffffffffu, a[kQPer - 1 - r], M);
@@ -101,7 +108,7 @@ __device__ __forceinline__ void q_mirror_shfl(float (&a)[kQPer], int lane, float
 }
 
 // cross-warp stage through shared memory: partner thread t ^ T; MIRROR reverses the registers
-// (mirror of merge size K: T = K/16 - 1, upper bit K/32).  `buf` alternates between the two
+// (mirror of merge size K: T = K/P - 1, upper bit K/2P).  `buf` alternates between the two
 // exchange buffers, so one barrier per stage suffices (a buffer is rewritten only after the
 // next stage's barrier, which every thread reaches after its reads of this one).
 template <int T, bool MIRROR>
@@ -110,13 +117,13 @@ __device__ __forceinline__ void q_stage_smem(float (&a)[kQPer], int t, float* xb
     float* s = xbuf + buf * kQChunk;
     buf ^= 1;
 #pragma unroll
-    for (int q = 0; q < 4; q++)
+    for (int q = 0; q < kQQuads; q++)
         *reinterpret_cast<float4*>(s + qslot(t, q)) = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
     __syncthreads();
     const int pt = t ^ T;
     float o[kQPer];
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
+    for (int q = 0; q < kQQuads; q++) {
         const float4 v = *reinterpret_cast<const float4*>(s + qslot(pt, q));
         o[4 * q] = v.x;
         o[4 * q + 1] = v.y;
@@ -143,19 +150,19 @@ __device__ __forceinline__ void q_cleaners_reg(float (&a)[kQPer]) {
     }
 }
 
-// half-cleaners of distance J, J/2, ..., 1 in layout L0 (key e = 16 t + r: J < 16 in registers,
-// J < 512 within the warp, else shared memory).  Cross-thread stages run in views; the view is
-// left (back to key space) before the first in-register stage.
+// half-cleaners of distance J, J/2, ..., 1 (key e = P t + r: J < P in registers, J < 32P within
+// the warp, else shared memory).  Cross-thread stages run in views; the view is left (back to
+// key space) before the first in-register stage.
 template <int J>
 __device__ __forceinline__ void q_cleaners(float (&a)[kQPer], QCtx& c, float& s_cur) {
     if constexpr (J >= 1) {
-        if constexpr (J < 16) {
+        if constexpr (J < kQPer) {
             q_scale(a, s_cur);
             s_cur = 1.0f;
             q_cleaners_reg<J>(a);
         } else {
-            if constexpr (J < 512) q_ce_shfl<J / 16>(a, c.lane, s_cur);
-            else q_stage_smem<J / 16, false>(a, c.t, c.xbuf, c.buf, s_cur);
+            if constexpr (J < 32 * kQPer) q_ce_shfl<J / kQPer>(a, c.lane, s_cur);
+            else q_stage_smem<J / kQPer, false>(a, c.t, c.xbuf, c.buf, s_cur);
             q_cleaners<J / 2>(a, c, s_cur);
         }
     }
@@ -166,9 +173,9 @@ template <int K>
 __device__ __forceinline__ void q_merges(float (&a)[kQPer], QCtx& c) {
     if constexpr (K <= kQChunk) {
         float s_cur = 1.0f;
-        if constexpr (K <= 16) q_mirror_reg<K>(a);
-        else if constexpr (K <= 512) q_mirror_shfl<K>(a, c.lane, s_cur);
-        else q_stage_smem<K / 16 - 1, true>(a, c.t, c.xbuf, c.buf, s_cur);
+        if constexpr (K <= kQPer) q_mirror_reg<K>(a);
+        else if constexpr (K <= 32 * kQPer) q_mirror_shfl<K>(a, c.lane, s_cur);
+        else q_stage_smem<K / kQPer - 1, true>(a, c.t, c.xbuf, c.buf, s_cur);
         q_cleaners<K / 4>(a, c, s_cur);
         q_merges<2 * K>(a, c);
     }
@@ -192,7 +199,10 @@ __global__ void __launch_bounds__(kQThreads, Q8_QT_MINB) sram_quantiles_kernel(c
     ctx.lane = lane;
     ctx.xbuf = xbuf;
     ctx.buf = 0;
-    double acc = 0.0, acc256 = 0.0;  // quantile j = t; thread 0 also owns j = 256
+    constexpr int kJ = (kQuantiles + kQThreads - 1) / kQThreads;  // quantiles j = t + k*T per thread
+    double acc[kJ];
+#pragma unroll
+    for (int k = 0; k < kJ; k++) acc[k] = 0.0;
     for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
         const int64_t base = c * kQChunk;
         const int64_t left = n - base;
@@ -202,7 +212,7 @@ __global__ void __launch_bounds__(kQThreads, Q8_QT_MINB) sram_quantiles_kernel(c
         // coalesced float4 loads, zeros canonicalized (-0 + 0 = +0), the chunk's tail padded
         // with +inf (never selected: every selected index is < m)
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
+        for (int q = 0; q < kQQuads; q++) {
             const int e = 4 * (t + kQThreads * q);
             if (e + 4 <= m) {
                 const float4 v = __ldcs(reinterpret_cast<const float4*>(x + base + e));
@@ -217,24 +227,27 @@ __global__ void __launch_bounds__(kQThreads, Q8_QT_MINB) sram_quantiles_kernel(c
             }
         }
         q_merges<2>(a, ctx);
-        // sorted: key e = 16 t + r is a[r] of thread t; publish and read the order statistics
+        // sorted: key e = P t + r is a[r] of thread t; publish and read the order statistics
         float* s = xbuf + ctx.buf * kQChunk;
         ctx.buf ^= 1;
 #pragma unroll
-        for (int q = 0; q < 4; q++)
+        for (int q = 0; q < kQQuads; q++)
             *reinterpret_cast<float4*>(s + qslot(t, q)) = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
         __syncthreads();
-        {
-            const int i = static_cast<int>((static_cast<int64_t>(t) * m) / kQuantiles);  // Q2
-            acc += static_cast<double>(s[qslot(i >> 4, (i >> 2) & 3) + (i & 3)]);
-        }
-        if (t == 0) {
-            const int i = static_cast<int>((256LL * m) / kQuantiles);
-            acc256 += static_cast<double>(s[qslot(i >> 4, (i >> 2) & 3) + (i & 3)]);
+#pragma unroll
+        for (int k = 0; k < kJ; k++) {
+            const int j = t + k * kQThreads;
+            if (j < kQuantiles) {
+                const int i = static_cast<int>((static_cast<int64_t>(j) * m) / kQuantiles);  // Q2
+                acc[k] += static_cast<double>(s[qslot(i / kQPer, (i % kQPer) >> 2) + (i & 3)]);
+            }
         }
     }
-    partial[static_cast<int64_t>(blockIdx.x) * kQuantiles + t] = acc;
-    if (t == 0) partial[static_cast<int64_t>(blockIdx.x) * kQuantiles + 256] = acc256;
+#pragma unroll
+    for (int k = 0; k < kJ; k++) {
+        const int j = t + k * kQThreads;
+        if (j < kQuantiles) partial[static_cast<int64_t>(blockIdx.x) * kQuantiles + j] = acc[k];
+    }
 }
 
 // ------------------------------------------------------------------ finalize (one CTA)
