@@ -518,6 +518,9 @@ def main():
             "e2e_resident_states": e2e_res, "zero1": zero1,
             "gpu_launches": args.steps, "clocks": clk.summary(),
             "achieved_gbs_whole_job": n_total * bpp / (ms_per_step / 1e3) / 1e9,
+            "paper_context": {"ms_per_update_per_1B_params": ms_per_step * 1e9 / n_total,
+                              "paper_8bit_adam_ms_per_1B": 47, "paper_8bit_momentum_ms_per_1B": 34,
+                              "paper_hardware": "V100, 32-bit gradients (T5, P:358-365); context, not the target"},
             "library": q8.version(),
         }
         print(json.dumps(out))

@@ -268,6 +268,14 @@ q8_status q8_optim8bit_step_zero_fused(q8_kind kind, q8_dtype g_dtype, int32_t w
  * (num_ctas 0 = the current device's SM count).  -1 on bad input. */
 int64_t q8_zero_signal_bytes(int32_t world, int32_t num_ctas);
 
+/* Count the non-finite gradient elements (NaN or +-inf) of g: *count_dev = #{i : g_i not finite}
+ * (failure detection: non-finite gradients are out of the step's contract, G13, so a
+ * mixed-precision caller skips the step when the count is non-zero, as AMP's GradScaler does).
+ *   g_dev      [n] gradients of g_dtype, 16-B aligned (read)
+ *   count_dev  one uint64 on the device, 8-B aligned (written: zeroed then accumulated on stream)
+ * Errors: INVALID for n < 0, NULL, misalignment or a bad dtype. */
+q8_status q8_count_nonfinite(const void* g_dev, q8_dtype g_dtype, int64_t n, uint64_t* count_dev, void* stream);
+
 /* Thread-local description of the last error ("" after success). */
 const char* q8_last_error(void);
 

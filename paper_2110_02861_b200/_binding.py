@@ -27,7 +27,7 @@ EXPORTS = ("q8_create_dynamic_codebook", "q8_create_linear_codebook", "q8_quanti
            "q8_optim8bit_step", "q8_optim8bit_step_multi", "q8_optim32bit_step_multi",
            "q8_optim8bit_step_layerwise", "q8_layerwise_workspace_bytes", "q8_optim8bit_step_zero_fused",
            "q8_zero_signal_bytes", "q8_estimate_quantiles", "q8_quantiles_workspace_bytes",
-           "q8_create_quantile_codebook", "q8_last_error", "q8_version")
+           "q8_create_quantile_codebook", "q8_count_nonfinite", "q8_last_error", "q8_version")
 
 
 class Q8Error(RuntimeError):
@@ -78,6 +78,7 @@ def _load():
     lib.q8_estimate_quantiles.argtypes = [vp, i64, vp, vp, vp, i64, vp]
     lib.q8_quantiles_workspace_bytes.argtypes = [i64]
     lib.q8_create_quantile_codebook.argtypes = [vp, vp]
+    lib.q8_count_nonfinite.argtypes = [vp, i32, i64, vp, vp]
     for f in EXPORTS[:-2]:
         getattr(lib, f).restype = ctypes.c_int
     lib.q8_layerwise_workspace_bytes.restype = i64
@@ -383,4 +384,16 @@ def create_quantile_codebook(quantiles) -> torch.Tensor:
         raise ValueError("need 257 quantiles")
     out = torch.empty(256, dtype=torch.float32)
     _check(lib.q8_create_quantile_codebook(q.data_ptr(), out.data_ptr()))
+    return out
+
+
+def count_nonfinite(g: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Number of NaN / inf elements of a gradient tensor, as a 1-element int64 CUDA tensor (no host
+    sync): the AMP-style guard before an 8-bit step (non-finite gradients are out of contract)."""
+    if g.dtype not in GDTYPES:
+        raise ValueError(f"unsupported gradient dtype {g.dtype}")
+    if out is None:
+        out = torch.empty(1, dtype=torch.int64, device=g.device)
+    _check(lib.q8_count_nonfinite(_dev_ptr(g, None, "g"), GDTYPES[g.dtype], g.numel(),
+                                  _dev_ptr(out, torch.int64, "out"), _stream(g.device)))
     return out

@@ -334,6 +334,33 @@ q8_status q8_create_quantile_codebook(const float* quantiles_host, float* out_ho
     return ok();
 }
 
+q8_status q8_count_nonfinite(const void* g_dev, q8_dtype g_dtype, int64_t n, uint64_t* count_dev, void* stream) {
+    if (n < 0) return fail(Q8_ERR_INVALID, "n < 0");
+    if (!count_dev) return fail(Q8_ERR_INVALID, "count_dev is NULL");
+    if (g_dtype != Q8_F32 && g_dtype != Q8_F16 && g_dtype != Q8_BF16) return fail(Q8_ERR_INVALID, "bad g_dtype %d", g_dtype);
+    if (n > 0 && !g_dev) return fail(Q8_ERR_INVALID, "NULL buffer with n > 0");
+    if (n > 0 && !aligned(g_dev, 16)) return fail(Q8_ERR_INVALID, "g not 16-byte aligned");
+    if (!aligned(count_dev, 8)) return fail(Q8_ERR_INVALID, "count_dev not 8-byte aligned");
+    DeviceState* d = nullptr;
+    if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(count_dev, 0, sizeof(uint64_t), st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(count)");
+    if (n == 0) return ok();
+    const int per = g_dtype == Q8_F32 ? 4 : 8;
+    const int64_t nv = (n / per + q8::kThreads - 1) / q8::kThreads;
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(nv, 4 * d->sms)));
+    auto* out = reinterpret_cast<unsigned long long*>(count_dev);
+    switch (g_dtype) {
+        case Q8_F32: q8::count_nonfinite_kernel<q8::G_F32><<<grid, q8::kThreads, 0, st>>>(g_dev, n, out); break;
+        case Q8_F16: q8::count_nonfinite_kernel<q8::G_F16><<<grid, q8::kThreads, 0, st>>>(g_dev, n, out); break;
+        case Q8_BF16: q8::count_nonfinite_kernel<q8::G_BF16><<<grid, q8::kThreads, 0, st>>>(g_dev, n, out); break;
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "count_nonfinite_kernel launch");
+    return ok();
+}
+
 q8_status q8_quantize_tensorwise(const float* code_dev, const float* x_dev, float* absmax_dev, uint8_t* codes_dev,
                                  int64_t n, void* stream) {
     if (n < 0) return fail(Q8_ERR_INVALID, "n < 0");

@@ -141,4 +141,49 @@ __global__ void __launch_bounds__(kThreads) dequantize_blockwise_kernel(const fl
     }
 }
 
+// Non-finite gradient count (failure detection: non-finite gradients are out of contract
+// for the step, G13; an AMP-style caller checks before stepping).  Bit tests on the raw encodings:
+// fp32 exponent 0xff, fp16 0x1f, bf16 0xff (NaN or +-inf).  16-byte vector loads, one 64-bit
+// atomic per CTA.
+template <int GDT>
+__global__ void __launch_bounds__(kThreads) count_nonfinite_kernel(const void* __restrict__ g, int64_t n,
+                                                                   unsigned long long* __restrict__ out) {
+    __shared__ unsigned int red[kWarps];
+    constexpr int kPer = GDT == G_F32 ? 4 : 8;  // elements per 16-byte load
+    unsigned int cnt = 0;
+    const int64_t nv = n / kPer;
+    const uint4* gv = static_cast<const uint4*>(g);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < nv;
+         i += static_cast<int64_t>(gridDim.x) * kThreads) {
+        const uint4 v = __ldcs(gv + i);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if constexpr (GDT == G_F32) {
+                cnt += ((w[k] & 0x7f800000u) == 0x7f800000u);
+            } else {
+                const uint32_t m = GDT == G_F16 ? 0x7c00u : 0x7f80u;
+                cnt += ((w[k] & m) == m) + (((w[k] >> 16) & m) == m);
+            }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < n - nv * kPer) {  // the tail (< kPer elements)
+        const int64_t i = nv * kPer + threadIdx.x;
+        if constexpr (GDT == G_F32) {
+            cnt += ((static_cast<const uint32_t*>(g)[i] & 0x7f800000u) == 0x7f800000u);
+        } else {
+            const uint32_t m = GDT == G_F16 ? 0x7c00u : 0x7f80u;
+            cnt += ((static_cast<const uint16_t*>(g)[i] & m) == m);
+        }
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int k = 0; k < kWarps; ++k) s += red[k];
+        if (s) atomicAdd(out, s);
+    }
+}
+
 }  // namespace q8

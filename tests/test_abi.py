@@ -157,3 +157,11 @@ def test_host_quantile_codebook_matches_oracle():
               np.linspace(0, 1, 257).astype(np.float32)):
         lib_c = B.create_quantile_codebook(torch.from_numpy(q)).numpy()
         np.testing.assert_array_equal(lib_c.view(np.uint32), oracle.quantile_codebook(q).view(np.uint32))
+
+
+def test_count_nonfinite_validation_without_device():
+    assert B.lib.q8_count_nonfinite(FAKE, B.Q8_BF16, -1, FAKE, None) == B.Q8_ERR_INVALID
+    assert B.lib.q8_count_nonfinite(FAKE, B.Q8_BF16, 10, None, None) == B.Q8_ERR_INVALID
+    assert B.lib.q8_count_nonfinite(None, B.Q8_F32, 10, FAKE, None) == B.Q8_ERR_INVALID
+    assert B.lib.q8_count_nonfinite(FAKE + 2, B.Q8_F16, 10, FAKE, None) == B.Q8_ERR_INVALID
+    assert B.lib.q8_count_nonfinite(FAKE, 7, 10, FAKE, None) == B.Q8_ERR_INVALID
