@@ -145,3 +145,27 @@ def test_layerwise_optimizer_api(q8, cls, kind):
     for p, r in zip(model.parameters(), ref):
         assert np.array_equal(p.detach().cpu().numpy().reshape(-1).view(np.uint32), r.view(np.uint32))
         assert "trust_scale" in opt.state[p]
+
+
+@pytest.mark.parametrize("i", range(8))
+def test_layerwise_random_sweep(q8, i):
+    # seeded random layer lists and hyper-parameters; the per-tensor scales come from binary64 norms
+    # summed in different orders (L3), so they are asserted within one fp32 ulp, and every tensor whose
+    # scale is identical must then match bit for bit
+    rng = np.random.default_rng(700 + i)
+    kind = ["lamb", "lars"][i % 2]
+    gdt = ["float32", "float16", "bfloat16"][i % 3]
+    sizes = [int(rng.integers(1, 40_000)) for _ in range(int(rng.integers(2, 30)))]
+    hp = dict(HP[kind])
+    hp.update(lr=float(10 ** rng.uniform(-4, -1)), weight_decay=float(rng.choice([0.0, 1e-4, 0.01])))
+    if kind == "lamb":
+        hp.update(beta2=float(rng.choice([0.99, 0.999])), bias_correction=bool(rng.integers(0, 2)))
+    ents, refs = _make(kind, sizes, gdt, seed0=1000 * i)
+    t = int(rng.integers(1, 20))
+    got, exp = _step_both(q8, kind, ents, refs, sizes, gdt, t, hp)
+    ulps = np.abs(got.view(np.int32).astype(np.int64) - exp.view(np.int32).astype(np.int64))
+    assert ulps.max() <= 1, (got, exp)
+    same = ulps == 0
+    sub_e = [e for e, s in zip(ents, same) if s]
+    sub_r = [r for r, s in zip(refs, same) if s]
+    _assert_equal(kind, sub_e, sub_r)
