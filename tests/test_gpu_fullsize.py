@@ -76,3 +76,52 @@ def test_full_size_momentum_multi_tensor_gpt2_medium_list():
             assert np.array_equal(p[b * B:min((b + 1) * B, n)].cpu().numpy().view(np.uint32), rp.view(np.uint32))
             assert np.array_equal(s1[b * B:min((b + 1) * B, n)].cpu().numpy(), rs)
             assert a1[b].item() == ra[0]
+
+
+def test_full_size_t5_11b_beyond_2_32_elements():
+    """BASELINE config 5 unsharded on one GPU: 11,307,321,344 parameters (> 2^32 elements: the 64-bit
+    element offsets of the kernel), 8-bit Adam, bf16 gradients, two steps from the zero state; sampled
+    blocks on both sides of 2^31 and 2^32 elements, random blocks, and the ragged last block."""
+    import paper_2110_02861_b200 as q8
+    workload = "cfg5_t5_11b"
+    kind = "adam"
+    hp = dict(synth.HPARAMS[kind])
+    n = synth.workload_numel(workload)
+    assert n > 2 ** 32
+    nb = (n + B - 1) // B
+    free, _ = torch.cuda.mem_get_info()
+    if free < n * 9.5:
+        pytest.skip(f"needs ~{n * 9.5 / 2**30:.0f} GiB of device memory")
+    p = torch.empty(n, dtype=torch.float32, device=DEV)
+    g = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    chunk = 1 << 28
+    for k, lo in enumerate(range(0, n, chunk)):  # seeded chunks (no full-size fp32 temporary)
+        hi = min(lo + chunk, n)
+        p[lo:hi] = synth.params(hi - lo, seed=500 + k, device=DEV)
+    s1, a1 = synth.zero_state(n, device=DEV)
+    s2, a2 = synth.zero_state(n, device=DEV)
+    rng = np.random.default_rng(11)
+    edges = [(2 ** 31) // B - 1, (2 ** 31) // B, (2 ** 32) // B - 1, (2 ** 32) // B]
+    blocks = sorted(set([0, nb - 1] + edges + rng.integers(0, nb, 24).tolist()))
+
+    def take(t, b):
+        return t[b * B:min((b + 1) * B, n)].cpu().numpy().copy()
+
+    ref = {b: dict(p=take(p, b), s1=take(s1, b), s2=take(s2, b), a1=a1[b:b + 1].cpu().numpy().copy(),
+                   a2=a2[b:b + 1].cpu().numpy().copy()) for b in blocks}
+    for t in (1, 2):
+        for k, lo in enumerate(range(0, n, chunk)):
+            hi = min(lo + chunk, n)
+            g[lo:hi] = synth.grads(hi - lo, step=t, seed=k, dtype="bfloat16", device=DEV)
+        q8.optim8bit_step(kind, p, g, s1, s2, a1, a2, step=t, **hp)
+        for b, r in ref.items():
+            oracle.optim8bit_step(kind, r["p"], synth.to_f32_numpy(g[b * B:min((b + 1) * B, n)]), r["s1"], r["s2"],
+                                  r["a1"], r["a2"], step=t, **hp)
+    torch.cuda.synchronize()
+    for b, r in ref.items():
+        assert np.array_equal(take(p, b).view(np.uint32), r["p"].view(np.uint32)), f"p block {b}"
+        assert np.array_equal(take(s1, b), r["s1"]), f"s1 block {b}"
+        assert np.array_equal(take(s2, b), r["s2"]), f"s2 block {b}"
+        assert a1[b].item() == r["a1"][0] and a2[b].item() == r["a2"][0], f"absmax block {b}"
+    del p, g, s1, s2, a1, a2
+    torch.cuda.empty_cache()
