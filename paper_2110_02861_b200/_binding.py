@@ -255,6 +255,20 @@ class TensorList:
                                      _dev_ptr(a1, torch.float32, "absmax1"), _dev_ptr(a2, torch.float32, "absmax2"), n)
         self.device = entries[0][0].device if entries else None
 
+    def update_grads(self, grads):
+        """Re-point the descriptors at this step's gradients (same count, sizes and dtype as
+        before); everything else (parameters, states) is unchanged, so no re-validation."""
+        if len(grads) != self.count:
+            raise ValueError("gradient count changed")
+        keep = list(self.keep)
+        for i, g in enumerate(grads):
+            p = keep[i][0]
+            if g.numel() != p.numel() or GDTYPES.get(g.dtype) != self.gdtype:
+                raise ValueError(f"tensor {i}: gradient size/dtype changed")
+            self.arr[i].g = _dev_ptr(g, None, "g")
+            keep[i] = (p, g) + tuple(keep[i][2:])
+        self.keep = keep
+
 
 def optim8bit_step_multi(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0,
                          bias_correction=True, step=1, blocksize=BLOCKSIZE, hp: HParams | None = None):

@@ -96,14 +96,19 @@ class _Optimizer8bit(torch.optim.Optimizer):
                         (p, g, st["s1"], st.get("s2"), st["absmax1"], st.get("absmax2")))
             b1, b2 = group["betas"]
             hp = B.hparams(group["lr"], b1, b2, group["eps"], group["weight_decay"], group["bias_correction"])
-            for (_, step), entries in buckets.items():
-                key = tuple(t.data_ptr() if t is not None else 0 for e in entries for t in e)
+            for (gdt, step), entries in buckets.items():
+                # descriptor arrays are cached per (group, dtype, parameter storage): a parameter whose
+                # .data is re-pointed gets a new key; states only change storage in load_state_dict,
+                # which clears the cache; gradients (re-allocated by backward) are refreshed each step
+                key = (id(group), gdt, tuple(e[0].data_ptr() for e in entries))
                 tl = self._lists.get(key)
                 if tl is None:
                     tl = B.TensorList(entries)
                     if len(self._lists) > 64:
                         self._lists.clear()
                     self._lists[key] = tl
+                else:
+                    tl.update_grads([e[1] for e in entries])
                 B.optim8bit_step_multi(self.kind, tl, lr=group["lr"], step=step, hp=hp)
             for (_, step), entries in buckets32.items():
                 B.optim32bit_step_multi(self.kind, entries, lr=group["lr"], step=step, hp=hp)

@@ -156,3 +156,33 @@ def test_stable_embedding_keeps_32bit_states(q8):
     assert "s1" in opt.state[lin.weight]
     for p, r in zip(params, ref):
         assert np.array_equal(p.detach().cpu().numpy().reshape(-1).view(np.uint32), r.view(np.uint32))
+
+
+def test_cached_descriptors_follow_new_storage(q8):
+    # the descriptor cache refreshes gradient pointers each step; a parameter whose .data is
+    # re-pointed between steps must be stepped in its new storage (and the old one left alone)
+    model = make_model()
+    opt = q8.AdamW8bit(model.parameters(), lr=1e-3)
+    x = torch.randn(16, 300, device=DEV)
+    ref = [p.detach().cpu().numpy().copy() for p in model.parameters()]
+    st = [dict(s1=np.zeros(p.size, np.uint8), s2=np.zeros(p.size, np.uint8),
+               a1=np.zeros((p.size + 2047) // 2048, np.float32), a2=np.zeros((p.size + 2047) // 2048, np.float32))
+          for p in ref]
+    hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, bias_correction=True)  # AdamW8bit defaults
+    old = None
+    for t in range(1, 4):
+        if t == 3:
+            p0 = next(model.parameters())
+            old = p0.data
+            p0.data = p0.data.clone()
+            old_copy = old.clone()
+        opt.zero_grad()
+        model(x).square().mean().backward()
+        grads = [p.grad.detach().cpu().numpy().copy() for p in model.parameters()]
+        opt.step()
+        for r, g, s in zip(ref, grads, st):
+            oracle.optim8bit_step("adamw", r.reshape(-1), g.reshape(-1), s["s1"], s["s2"], s["a1"], s["a2"], step=t, **hp)
+    torch.cuda.synchronize()
+    for p, r in zip(model.parameters(), ref):
+        assert np.array_equal(p.detach().cpu().numpy().view(np.uint32), r.view(np.uint32))
+    assert torch.equal(old, old_copy)  # the abandoned storage was not written
