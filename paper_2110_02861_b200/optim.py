@@ -55,6 +55,21 @@ class _Optimizer8bit(torch.optim.Optimizer):
                     st["absmax2"] = torch.zeros(nb, dtype=torch.float32, device=p.device)
         return st
 
+    def _tensor_list(self, group, gdt, entries):
+        """The multi-tensor descriptor array for these entries, cached per (group, dtype, parameter
+        storage): a parameter whose .data is re-pointed gets a new key; states only change storage in
+        load_state_dict, which clears the cache; gradients (re-allocated by backward) are refreshed."""
+        key = (id(group), gdt, tuple(e[0].data_ptr() for e in entries))
+        tl = self._lists.get(key)
+        if tl is None:
+            tl = B.TensorList(entries)
+            if len(self._lists) > 64:
+                self._lists.clear()
+            self._lists[key] = tl
+        else:
+            tl.update_grads([e[1] for e in entries])
+        return tl
+
     def load_state_dict(self, state_dict):
         # torch casts floating-point-param state to the param dtype; codes must stay uint8
         super().load_state_dict(state_dict)
@@ -97,18 +112,7 @@ class _Optimizer8bit(torch.optim.Optimizer):
             b1, b2 = group["betas"]
             hp = B.hparams(group["lr"], b1, b2, group["eps"], group["weight_decay"], group["bias_correction"])
             for (gdt, step), entries in buckets.items():
-                # descriptor arrays are cached per (group, dtype, parameter storage): a parameter whose
-                # .data is re-pointed gets a new key; states only change storage in load_state_dict,
-                # which clears the cache; gradients (re-allocated by backward) are refreshed each step
-                key = (id(group), gdt, tuple(e[0].data_ptr() for e in entries))
-                tl = self._lists.get(key)
-                if tl is None:
-                    tl = B.TensorList(entries)
-                    if len(self._lists) > 64:
-                        self._lists.clear()
-                    self._lists[key] = tl
-                else:
-                    tl.update_grads([e[1] for e in entries])
+                tl = self._tensor_list(group, gdt, entries)
                 B.optim8bit_step_multi(self.kind, tl, lr=group["lr"], step=step, hp=hp)
             for (_, step), entries in buckets32.items():
                 B.optim32bit_step_multi(self.kind, entries, lr=group["lr"], step=step, hp=hp)
@@ -170,8 +174,8 @@ class _LayerwiseOptimizer8bit(_Optimizer8bit):
             b1, b2 = group["betas"]
             hp = B.hparams(group["lr"], b1, b2, group["eps"], group["weight_decay"], group["bias_correction"])
             eta = group.get("trust_coefficient", self.trust_coefficient)
-            for (_, step), entries in buckets.items():
-                tl = B.TensorList(entries)
+            for (gdt, step), entries in buckets.items():
+                tl = self._tensor_list(group, gdt, entries)
                 need = B.layerwise_workspace_bytes(tl)
                 if self._workspace is None or self._workspace.numel() < need:
                     self._workspace = torch.empty(need, dtype=torch.uint8, device=tl.device)
