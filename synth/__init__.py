@@ -83,6 +83,9 @@ WORKLOADS = {
     # ratio per tensor), measured with the same bench contract
     "lamb_gpt2_xl": dict(kind="lamb", grad_dtype="bfloat16", shapes=gpt2_shapes(1600, 48), layerwise=True,
                          desc="8-bit LAMB, GPT-2-XL 580-tensor layer list, bf16 grads"),
+    # the user-facing torch.optim API ("two-line change", P:7) over a real parameter list
+    "optim_api_gpt2_xl": dict(kind="adamw", grad_dtype="bfloat16", shapes=gpt2_shapes(1600, 48), optim_api=True,
+                              desc="AdamW8bit.step() over GPT-2-XL's 580 parameter tensors, bf16 grads"),
     # SURVEY 8(f) row 4 (App G): SRAM-Quantiles over a GPT-2-XL-sized fp32 buffer
     "quantiles_gpt2_xl": dict(kind="adamw", grad_dtype="float32", shapes=gpt2_shapes(1600, 48), quantiles=True,
                               desc="SRAM-Quantiles + Eq.5 codebook over a 1.5B fp32 GPT-2-XL-sized buffer"),
