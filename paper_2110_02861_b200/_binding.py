@@ -260,14 +260,12 @@ class TensorList:
         before); everything else (parameters, states) is unchanged, so no re-validation."""
         if len(grads) != self.count:
             raise ValueError("gradient count changed")
-        keep = list(self.keep)
+        arr, gd = self.arr, self.gdtype
         for i, g in enumerate(grads):
-            p = keep[i][0]
-            if g.numel() != p.numel() or GDTYPES.get(g.dtype) != self.gdtype:
-                raise ValueError(f"tensor {i}: gradient size/dtype changed")
-            self.arr[i].g = _dev_ptr(g, None, "g")
-            keep[i] = (p, g) + tuple(keep[i][2:])
-        self.keep = keep
+            if not g.is_cuda or GDTYPES.get(g.dtype) != gd or g.numel() != arr[i].n:
+                raise ValueError(f"tensor {i}: gradient device/size/dtype changed")
+            arr[i].g = g.data_ptr()
+        self.grads = grads  # keep this step's gradients alive until the next refresh
 
 
 def optim8bit_step_multi(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0,
