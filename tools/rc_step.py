@@ -1,3 +1,4 @@
+"""Racecheck helper: two fused steps on an n-element flat buffer (usage: rc_step.py n kind)."""
 import sys, torch
 sys.path.insert(0, '.')
 import paper_2110_02861_b200 as q8, synth
