@@ -860,7 +860,8 @@ def main_quantiles(args, cfg, q8, world, rank, local, dev):
     buffer (the parameters, N(0, 0.02^2)) plus the Eq.5 codebook; a step is one
     q8_estimate_quantiles call (sort/accumulate pass + finalize).  Independent problems per GPU
     (weak scaling replicas).  The roofline is the ALU issue rate: the kernel sorts every 4096-value
-    chunk on chip with a 78-stage bitonic network (one min-or-max per key per stage)."""
+    chunk's halves on chip with a 66-stage bitonic network (one min-or-max per key per stage) and selects
+    the 257 order statistics by merge-path binary search."""
     n = cfg["n_params"]
     x = synth.params(n, seed=1 + rank, device=dev)
     ws = torch.empty(q8.quantiles_workspace_bytes(n), dtype=torch.uint8, device=dev)
@@ -890,7 +891,9 @@ def main_quantiles(args, cfg, q8, world, rank, local, dev):
     ms_per_step = float(ms[0])
     clocks = clk.summary()
     sm_max = clocks.get("sm_max_mhz") or 1965.0
-    ops_per_elem = 78  # bitonic stages for 4096 keys: 12*13/2, one min-or-max per key per stage
+    # the comparator network the kernel runs: bitonic merges up to runs of 2048 (11*12/2 = 66 stages,
+    # one min-or-max per key per stage); the last merge is replaced by per-quantile selection
+    ops_per_elem = 66
     # min/max (IMNMX) issue on the ALU pipe: rt_SMSP = 2 cycles per warp instruction (B300_MICROARCH.md
     # "Pipe rates"), i.e. 16 lanes/clk per SMSP, 64 per SM; 148 SMs (B200_PROFILING.md)
     peak_ops = 148 * 4 * 16 * sm_max * 1e6 / 1e12

@@ -169,15 +169,50 @@ __device__ __forceinline__ void q_cleaners(float (&a)[kQPer], QCtx& c, float& s_
 }
 
 // bitonic merges of size K, 2K, ..., 4096 (flip form: mirror stage, then half-cleaners)
+// The network sorts the two halves of the chunk (merges up to kQSortK = 2048); the last merge is
+// replaced by selection: each wanted order statistic is found by one merge-path binary search over
+// the two sorted halves (q_select), which costs ~12 shared loads per quantile instead of the 12
+// network stages of the final merge for every key.
+#ifndef Q8_QT_SELECT
+#define Q8_QT_SELECT 1
+#endif
+constexpr int kQSortK = Q8_QT_SELECT ? kQChunk / 2 : kQChunk;
+
 template <int K>
 __device__ __forceinline__ void q_merges(float (&a)[kQPer], QCtx& c) {
-    if constexpr (K <= kQChunk) {
+    if constexpr (K <= kQSortK) {
         float s_cur = 1.0f;
         if constexpr (K <= kQPer) q_mirror_reg<K>(a);
         else if constexpr (K <= 32 * kQPer) q_mirror_shfl<K>(a, c.lane, s_cur);
         else q_stage_smem<K / kQPer - 1, true>(a, c.t, c.xbuf, c.buf, s_cur);
         q_cleaners<K / 4>(a, c, s_cur);
         q_merges<2 * K>(a, c);
+    }
+}
+
+// word of key e in an exchange buffer (the layout q_stage_smem / the publish step write)
+__device__ __forceinline__ int qword(int e) { return qslot(e / kQPer, (e % kQPer) >> 2) + (e & 3); }
+
+// The value of rank i (0-based) of the chunk.  Without selection the buffer holds the sorted chunk.
+// With it, it holds two ascending runs A = [0, H), B = [H, 2H) (H = kQChunk/2): the element of rank
+// i of their merge is the last of the first D = i+1 merged elements; with a = #A-elements among them
+// (the merge path: A[a-1] <= B[D-a] and B[D-1-a] < A[a], ties taken from A first) it is
+// max(A[a-1], B[D-1-a]).  Equal values make the tie rule irrelevant: the value is unique (Q2).
+__device__ __forceinline__ float q_select(const float* s, int i) {
+    if constexpr (!Q8_QT_SELECT) {
+        return s[qword(i)];
+    } else {
+        constexpr int H = kQChunk / 2;
+        const int D = i + 1;
+        int lo = D > H ? D - H : 0, hi = D < H ? D : H;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (s[qword(mid)] <= s[qword(H + D - 1 - mid)]) lo = mid + 1;
+            else hi = mid;
+        }
+        const float x = lo > 0 ? s[qword(lo - 1)] : -__int_as_float(0x7f800000);
+        const float y = D - lo > 0 ? s[qword(H + D - 1 - lo)] : -__int_as_float(0x7f800000);
+        return fmaxf(x, y);
     }
 }
 
@@ -227,7 +262,8 @@ __global__ void __launch_bounds__(kQThreads, Q8_QT_MINB) sram_quantiles_kernel(c
             }
         }
         q_merges<2>(a, ctx);
-        // sorted: key e = P t + r is a[r] of thread t; publish and read the order statistics
+        // sorted runs of kQSortK: key e = P t + r is a[r] of thread t; publish and read the order
+        // statistics
         float* s = xbuf + ctx.buf * kQChunk;
         ctx.buf ^= 1;
 #pragma unroll
@@ -239,7 +275,7 @@ __global__ void __launch_bounds__(kQThreads, Q8_QT_MINB) sram_quantiles_kernel(c
             const int j = t + k * kQThreads;
             if (j < kQuantiles) {
                 const int i = static_cast<int>((static_cast<int64_t>(j) * m) / kQuantiles);  // Q2
-                acc[k] += static_cast<double>(s[qslot(i / kQPer, (i % kQPer) >> 2) + (i & 3)]);
+                acc[k] += static_cast<double>(q_select(s, i));
             }
         }
     }
