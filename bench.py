@@ -898,6 +898,11 @@ def main_quantiles(args, cfg, q8, world, rank, local, dev):
     # "Pipe rates"), i.e. 16 lanes/clk per SMSP, 64 per SM; 148 SMs (B200_PROFILING.md)
     peak_ops = 148 * 4 * 16 * sm_max * 1e6 / 1e12
     achieved = n * ops_per_elem / (ms_per_step / 1e3) / 1e12
+    traffic = None  # DRAM bytes per launch from the committed ncu capture (4 B/element read)
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if world == 1 and os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
@@ -921,7 +926,7 @@ def main_quantiles(args, cfg, q8, world, rank, local, dev):
             "data": "synthetic: x ~ N(0, 0.02^2) fp32 (the GPT-2-XL-sized parameter buffer)",
             "config": cfg,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_ops, "unit": "Tops/s",
-                         "frac": achieved / peak_ops, "traffic": None, "ops_per_element": ops_per_elem,
+                         "frac": achieved / peak_ops, "traffic": traffic, "ops_per_element": ops_per_elem,
                          "kernel": "sram_quantiles_kernel (+ one-CTA finalize)",
                          "peak_source": "ALU pipe: 148 SMs x 4 SMSPs x 16 lanes/clk (rt_SMSP=2) x sm_max clock",
                          "hbm_gbs": n * 4 / (ms_per_step / 1e3) / 1e9},
