@@ -165,3 +165,21 @@ def test_count_nonfinite_validation_without_device():
     assert B.lib.q8_count_nonfinite(None, B.Q8_F32, 10, FAKE, None) == B.Q8_ERR_INVALID
     assert B.lib.q8_count_nonfinite(FAKE + 2, B.Q8_F16, 10, FAKE, None) == B.Q8_ERR_INVALID
     assert B.lib.q8_count_nonfinite(FAKE, 7, 10, FAKE, None) == B.Q8_ERR_INVALID
+
+
+def test_binding_rejects_bad_tensors_before_the_c_call():
+    # argument marshalling checks in the Python binding (no device needed): CPU tensors, sizes, dtypes
+    p = torch.zeros(4096)
+    g = torch.zeros(4096, dtype=torch.bfloat16)
+    s = torch.zeros(4096, dtype=torch.uint8)
+    a = torch.zeros(2)
+    with pytest.raises(ValueError, match="CUDA"):
+        q8.optim8bit_step("adamw", p, g, s, s.clone(), a, a.clone(), lr=1e-3, step=1)
+    with pytest.raises(ValueError, match="size mismatch"):
+        q8.optim8bit_step("adamw", p, g[:100], s, s.clone(), a, a.clone(), lr=1e-3, step=1)
+    with pytest.raises(ValueError, match="unsupported gradient dtype"):
+        q8.optim8bit_step("adam", p, g.to(torch.float64), s, s.clone(), a, a.clone(), lr=1e-3, step=1)
+    with pytest.raises(ValueError):
+        q8.count_nonfinite(torch.zeros(8, dtype=torch.int32))
+    with pytest.raises(ValueError, match="257"):
+        q8.create_quantile_codebook(torch.zeros(10))
