@@ -29,7 +29,14 @@ constexpr int kWarps = kThreads / 32;
 enum { KIND_ADAM = 0, KIND_ADAMW = 1, KIND_MOMENTUM = 2, KIND_LAMB = 3, KIND_LARS = 4 };
 // Kinds with two states (s1 signed, s2 unsigned): the Adam family and LAMB; Momentum and LARS
 // keep one (the momentum buffer, signed table).
-__host__ __device__ constexpr bool two_states(int kind) { return kind != KIND_MOMENTUM && kind != KIND_LARS; }
+// Kernel-only flag on KIND_ADAM / KIND_MOMENTUM: the L2 weight-decay term g += wd*w (G10) is on
+// (wd != 0).  The launchers pick it from the host hyper-parameters, so the step kernel carries no
+// per-element run-time test for it.
+constexpr int KIND_L2 = 8;
+__host__ __device__ constexpr int kind_base(int kind) { return kind & 7; }
+__host__ __device__ constexpr bool two_states(int kind) {
+    return kind_base(kind) != KIND_MOMENTUM && kind_base(kind) != KIND_LARS;
+}
 enum { G_F32 = 0, G_F16 = 1, G_BF16 = 2 };
 
 // Device-resident immutable tables (built on the host, codebook_host.cpp), as fp32 words:

@@ -55,9 +55,12 @@ cudaError_t launch_kind(const StepParams<MAXT>& P, const LaunchCtx& ctx) {
 template <int MAXT>
 cudaError_t launch_any(int kind, const StepParams<MAXT>& P, const LaunchCtx& ctx) {
     switch (kind) {
-        case KIND_ADAM: return launch_kind<KIND_ADAM, MAXT>(P, ctx);
+        case KIND_ADAM:
+            return P.s.wd != 0.0f ? launch_kind<KIND_ADAM | KIND_L2, MAXT>(P, ctx) : launch_kind<KIND_ADAM, MAXT>(P, ctx);
         case KIND_ADAMW: return launch_kind<KIND_ADAMW, MAXT>(P, ctx);
-        case KIND_MOMENTUM: return launch_kind<KIND_MOMENTUM, MAXT>(P, ctx);
+        case KIND_MOMENTUM:
+            return P.s.wd != 0.0f ? launch_kind<KIND_MOMENTUM | KIND_L2, MAXT>(P, ctx)
+                                  : launch_kind<KIND_MOMENTUM, MAXT>(P, ctx);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -139,9 +142,12 @@ cudaError_t launch_zero_t(const StepParams<1>& P, const LaunchCtx& ctx, int grid
 
 cudaError_t Q8_CAT(launch_zero_g, Q8_GDT)(int kind, const StepParams<1>& P, const LaunchCtx& ctx, int grid) {
     switch (kind) {
-        case KIND_ADAM: return launch_zero_t<KIND_ADAM>(P, ctx, grid);
+        case KIND_ADAM:
+            return P.s.wd != 0.0f ? launch_zero_t<KIND_ADAM | KIND_L2>(P, ctx, grid) : launch_zero_t<KIND_ADAM>(P, ctx, grid);
         case KIND_ADAMW: return launch_zero_t<KIND_ADAMW>(P, ctx, grid);
-        case KIND_MOMENTUM: return launch_zero_t<KIND_MOMENTUM>(P, ctx, grid);
+        case KIND_MOMENTUM:
+            return P.s.wd != 0.0f ? launch_zero_t<KIND_MOMENTUM | KIND_L2>(P, ctx, grid)
+                                  : launch_zero_t<KIND_MOMENTUM>(P, ctx, grid);
         default: return cudaErrorInvalidValue;
     }
 }
