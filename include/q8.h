@@ -81,9 +81,10 @@ typedef struct {
  * rounded once to fp32.  Pure host function.  Errors: INVALID if out_host is NULL. */
 q8_status q8_create_dynamic_codebook(int32_t is_signed, float* out_host);
 
-/* Fill out_host[256] with the linear data type: 256 evenly spaced values over [-1, 1]
- * (is_signed = 1; -1 + 2i/255) or [0, 1] (is_signed = 0; i/255), computed in double and rounded
- * once.  The paper's ablation baseline "without dynamic quantization use linear quantization"
+/* Fill out_host[256] with the linear data type: 256 evenly spaced values, signed
+ * (is_signed = 1) (i - 127)/128 over [-127/128, 1] with an exact 0 at index 127 (reading L0,
+ * zero states must round-trip exactly), unsigned (is_signed = 0) i/255 over [0, 1];
+ * computed in double and rounded once.  The paper's ablation baseline "without dynamic quantization use linear quantization"
  * (T3 caption).  Pure host function.  Errors: INVALID if out_host is NULL. */
 q8_status q8_create_linear_codebook(int32_t is_signed, float* out_host);
 

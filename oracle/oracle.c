@@ -125,12 +125,15 @@ int oracle_dynamic_codebook(int is_signed, float out[256]) {
 
 /*
  * Linear data type (the ablation baseline "without dynamic quantization use linear
- * quantization", T3 caption P:214): 256 evenly spaced values, -1 + 2i/255 (signed) or i/255
- * (unsigned), i = 0..255, evaluated in double and rounded once to binary32.
+ * quantization", T3 caption P:214): 256 evenly spaced values.  Reading L0: the
+ * paper gives no formula; 256 evenly spaced values cannot be symmetric AND contain 0, and an
+ * optimizer state needs an exact 0 (Eq.2 "r_0 = m_0 = 0"), so the signed type is
+ * (i - 127)/128 -- exact 0 at index 127 and +1 at 255, the dynamic type's layout of its
+ * specials -- and the unsigned type i/255, i = 0..255; evaluated in double, rounded once.
  */
 int oracle_linear_codebook(int is_signed, float out[256]) {
     for (int i = 0; i < 256; i++) {
-        double v = is_signed ? -1.0 + 2.0 * (double)i / 255.0 : (double)i / 255.0;
+        double v = is_signed ? (double)(i - 127) / 128.0 : (double)i / 255.0;
         out[i] = (float)v;
     }
     return 0;

@@ -101,7 +101,9 @@ def _stream(device=None) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
-def _dev_ptr(t: torch.Tensor | None, dtype=None, name="tensor") -> int | None:
+def _dev_ptr(t: torch.Tensor | None, dtype=None, name="tensor", device=None) -> int | None:
+    """Device address of a contiguous CUDA tensor; `device` (if given) is the device of the call:
+    every buffer of one call must live on it (the C ABI launches on the current device)."""
     if t is None:
         return None
     if not t.is_cuda:
@@ -110,7 +112,17 @@ def _dev_ptr(t: torch.Tensor | None, dtype=None, name="tensor") -> int | None:
         raise ValueError(f"{name} must be contiguous")
     if dtype is not None and t.dtype != dtype:
         raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, but this call runs on {device}")
     return t.data_ptr()
+
+
+def _on(device):
+    """Make `device` current for one C call: the library takes its tables, SM count and launch
+    device from the current CUDA device, and the stream handle is that device's current stream."""
+    if torch.device(device).type != "cuda":
+        raise ValueError(f"the 8-bit kernels take CUDA tensors (got a tensor on {device})")
+    return torch.cuda.device(device)
 
 
 def version() -> str:
@@ -138,73 +150,81 @@ def create_linear_codebook(signed: bool) -> torch.Tensor:
 def quantize_tensorwise(code: torch.Tensor, x: torch.Tensor, absmax: torch.Tensor | None = None,
                         codes: torch.Tensor | None = None):
     """Eq.3: one absmax for the whole tensor, then the nearest code of x/N."""
-    n = x.numel()
+    n, dev = x.numel(), x.device
     if absmax is None:
-        absmax = torch.empty(1, dtype=torch.float32, device=x.device)
+        absmax = torch.empty(1, dtype=torch.float32, device=dev)
     if codes is None:
-        codes = torch.empty(n, dtype=torch.uint8, device=x.device)
+        codes = torch.empty(n, dtype=torch.uint8, device=dev)
     if codes.numel() != n or absmax.numel() < 1 or code.numel() != 256:
         raise ValueError("size mismatch")
-    _check(lib.q8_quantize_tensorwise(_dev_ptr(code, torch.float32, "code"), _dev_ptr(x, torch.float32, "x"),
-                                      _dev_ptr(absmax, torch.float32, "absmax"), _dev_ptr(codes, torch.uint8, "codes"),
-                                      n, _stream(x.device)))
+    with _on(dev):
+        _check(lib.q8_quantize_tensorwise(_dev_ptr(code, torch.float32, "code", dev), _dev_ptr(x, torch.float32, "x"),
+                                          _dev_ptr(absmax, torch.float32, "absmax", dev),
+                                          _dev_ptr(codes, torch.uint8, "codes", dev), n, _stream(dev)))
     return absmax, codes
 
 
 def dequantize_tensorwise(code: torch.Tensor, codes: torch.Tensor, absmax: torch.Tensor,
                           out: torch.Tensor | None = None):
-    n = codes.numel()
+    n, dev = codes.numel(), codes.device
     if out is None:
-        out = torch.empty(n, dtype=torch.float32, device=codes.device)
+        out = torch.empty(n, dtype=torch.float32, device=dev)
     if out.numel() != n or absmax.numel() < 1 or code.numel() != 256:
         raise ValueError("size mismatch")
-    _check(lib.q8_dequantize_tensorwise(_dev_ptr(code, torch.float32, "code"), _dev_ptr(codes, torch.uint8, "codes"),
-                                        _dev_ptr(absmax, torch.float32, "absmax"), _dev_ptr(out, torch.float32, "out"),
-                                        n, _stream(codes.device)))
+    with _on(dev):
+        _check(lib.q8_dequantize_tensorwise(_dev_ptr(code, torch.float32, "code", dev),
+                                            _dev_ptr(codes, torch.uint8, "codes"),
+                                            _dev_ptr(absmax, torch.float32, "absmax", dev),
+                                            _dev_ptr(out, torch.float32, "out", dev), n, _stream(dev)))
     return out
 
 
 def quantize_blockwise(code: torch.Tensor, x: torch.Tensor, absmax: torch.Tensor | None = None,
                        codes: torch.Tensor | None = None, blocksize: int = BLOCKSIZE):
-    n = x.numel()
+    n, dev = x.numel(), x.device
     if absmax is None:
-        absmax = torch.empty(nblocks(n, blocksize), dtype=torch.float32, device=x.device)
+        absmax = torch.empty(nblocks(n, blocksize), dtype=torch.float32, device=dev)
     if codes is None:
-        codes = torch.empty(n, dtype=torch.uint8, device=x.device)
+        codes = torch.empty(n, dtype=torch.uint8, device=dev)
     if codes.numel() != n or absmax.numel() < nblocks(n, blocksize) or code.numel() != 256:
         raise ValueError("size mismatch")
-    _check(lib.q8_quantize_blockwise(_dev_ptr(code, torch.float32, "code"), _dev_ptr(x, torch.float32, "x"),
-                                     _dev_ptr(absmax, torch.float32, "absmax"),
-                                     _dev_ptr(codes, torch.uint8, "codes"), n, blocksize, _stream(x.device)))
+    with _on(dev):
+        _check(lib.q8_quantize_blockwise(_dev_ptr(code, torch.float32, "code", dev), _dev_ptr(x, torch.float32, "x"),
+                                         _dev_ptr(absmax, torch.float32, "absmax", dev),
+                                         _dev_ptr(codes, torch.uint8, "codes", dev), n, blocksize, _stream(dev)))
     return absmax, codes
 
 
 def quantize_blockwise_dynamic(signed: bool, x: torch.Tensor, absmax: torch.Tensor | None = None,
                                codes: torch.Tensor | None = None, blocksize: int = BLOCKSIZE):
     """Eq.4 with the library's built-in dynamic data type (the step kernel's search path)."""
-    n = x.numel()
+    n, dev = x.numel(), x.device
     if absmax is None:
-        absmax = torch.empty(nblocks(n, blocksize), dtype=torch.float32, device=x.device)
+        absmax = torch.empty(nblocks(n, blocksize), dtype=torch.float32, device=dev)
     if codes is None:
-        codes = torch.empty(n, dtype=torch.uint8, device=x.device)
+        codes = torch.empty(n, dtype=torch.uint8, device=dev)
     if codes.numel() != n or absmax.numel() < nblocks(n, blocksize):
         raise ValueError("size mismatch")
-    _check(lib.q8_quantize_blockwise_dynamic(1 if signed else 0, _dev_ptr(x, torch.float32, "x"),
-                                             _dev_ptr(absmax, torch.float32, "absmax"),
-                                             _dev_ptr(codes, torch.uint8, "codes"), n, blocksize, _stream(x.device)))
+    with _on(dev):
+        _check(lib.q8_quantize_blockwise_dynamic(1 if signed else 0, _dev_ptr(x, torch.float32, "x"),
+                                                 _dev_ptr(absmax, torch.float32, "absmax", dev),
+                                                 _dev_ptr(codes, torch.uint8, "codes", dev), n, blocksize,
+                                                 _stream(dev)))
     return absmax, codes
 
 
 def dequantize_blockwise(code: torch.Tensor, codes: torch.Tensor, absmax: torch.Tensor,
                          out: torch.Tensor | None = None, blocksize: int = BLOCKSIZE):
-    n = codes.numel()
+    n, dev = codes.numel(), codes.device
     if out is None:
-        out = torch.empty(n, dtype=torch.float32, device=codes.device)
+        out = torch.empty(n, dtype=torch.float32, device=dev)
     if out.numel() != n or absmax.numel() < nblocks(n, blocksize) or code.numel() != 256:
         raise ValueError("size mismatch")
-    _check(lib.q8_dequantize_blockwise(_dev_ptr(code, torch.float32, "code"), _dev_ptr(codes, torch.uint8, "codes"),
-                                       _dev_ptr(absmax, torch.float32, "absmax"), _dev_ptr(out, torch.float32, "out"),
-                                       n, blocksize, _stream(codes.device)))
+    with _on(dev):
+        _check(lib.q8_dequantize_blockwise(_dev_ptr(code, torch.float32, "code", dev),
+                                           _dev_ptr(codes, torch.uint8, "codes"),
+                                           _dev_ptr(absmax, torch.float32, "absmax", dev),
+                                           _dev_ptr(out, torch.float32, "out", dev), n, blocksize, _stream(dev)))
     return out
 
 
@@ -213,56 +233,78 @@ def hparams(lr, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, bias_correct
                    1 if bias_correction else 0)
 
 
+def _check_state_sizes(i, n, kind, g, s1, s2, a1, a2):
+    """Sizes the C ABI cannot see: every buffer of a tensor holds n elements (absmax: one per
+    2048-block), and the second state exists exactly for the two-state kinds."""
+    two = kind in (Q8_ADAM, Q8_ADAMW, Q8_LAMB)
+    nb = nblocks(n)
+    if g.numel() != n or s1.numel() != n or a1.numel() < nb:
+        raise ValueError(f"tensor {i}: size mismatch (g, s1 need {n} elements, absmax1 {nb})")
+    if two and (s2 is None or a2 is None or s2.numel() != n or a2.numel() < nb):
+        raise ValueError(f"tensor {i}: size mismatch (s2 needs {n} elements, absmax2 {nb})")
+
+
 def optim8bit_step(kind, p, g, s1, s2, absmax1, absmax2, *, lr, beta1=0.9, beta2=0.999, eps=1e-8,
                    weight_decay=0.0, bias_correction=True, step=1, blocksize=BLOCKSIZE, hp: HParams | None = None):
     """One fused 8-bit step on a single flat tensor (in place)."""
     kind = KINDS.get(kind, kind)
-    n = p.numel()
-    if g.numel() != n or s1.numel() != n or (kind in (Q8_ADAM, Q8_ADAMW) and s2.numel() != n):
-        raise ValueError("size mismatch")
+    n, dev = p.numel(), p.device
+    _check_state_sizes(0, n, kind, g, s1, s2, absmax1, absmax2)
     if g.dtype not in GDTYPES:
         raise ValueError(f"unsupported gradient dtype {g.dtype}")
     if hp is None:
         hp = hparams(lr, beta1, beta2, eps, weight_decay, bias_correction)
-    _check(lib.q8_optim8bit_step(kind, _dev_ptr(p, torch.float32, "p"), _dev_ptr(g, None, "g"), GDTYPES[g.dtype],
-                                 _dev_ptr(s1, torch.uint8, "s1"), _dev_ptr(s2, torch.uint8, "s2"),
-                                 _dev_ptr(absmax1, torch.float32, "absmax1"),
-                                 _dev_ptr(absmax2, torch.float32, "absmax2"), n, blocksize, ctypes.byref(hp),
-                                 int(step), _stream(p.device)))
+    with _on(dev):
+        _check(lib.q8_optim8bit_step(kind, _dev_ptr(p, torch.float32, "p"), _dev_ptr(g, None, "g", dev),
+                                     GDTYPES[g.dtype], _dev_ptr(s1, torch.uint8, "s1", dev),
+                                     _dev_ptr(s2, torch.uint8, "s2", dev),
+                                     _dev_ptr(absmax1, torch.float32, "absmax1", dev),
+                                     _dev_ptr(absmax2, torch.float32, "absmax2", dev), n, blocksize, ctypes.byref(hp),
+                                     int(step), _stream(dev)))
 
 
 class TensorList:
     """A prepared (cached) host descriptor array for optim8bit_step_multi."""
 
-    def __init__(self, entries):
-        """entries: iterable of (p, g, s1, s2_or_None, absmax1, absmax2_or_None) CUDA tensors."""
+    def __init__(self, entries, kind=None):
+        """entries: iterable of (p, g, s1, s2_or_None, absmax1, absmax2_or_None) CUDA tensors, all on
+        one device.  kind (optional): checks that the second state is present for Adam/AdamW/LAMB."""
         entries = list(entries)
         self.arr = (TensorDesc * max(1, len(entries)))()
         self.count = len(entries)
         self.gdtype = None
         self.keep = entries  # keep tensors alive
+        self.device = entries[0][0].device if entries else None
+        kind = KINDS.get(kind, kind)
+        dev = self.device
         for i, (p, g, s1, s2, a1, a2) in enumerate(entries):
             n = p.numel()
-            if g.numel() != n or s1.numel() != n or (s2 is not None and s2.numel() != n):
+            if kind is not None:
+                _check_state_sizes(i, n, kind, g, s1, s2, a1, a2)
+            elif g.numel() != n or s1.numel() != n or a1.numel() < nblocks(n) or \
+                    (s2 is not None and (s2.numel() != n or a2 is None or a2.numel() < nblocks(n))):
                 raise ValueError(f"tensor {i}: size mismatch")
+            if g.dtype not in GDTYPES:
+                raise ValueError(f"tensor {i}: unsupported gradient dtype {g.dtype}")
             gd = GDTYPES[g.dtype]
             if self.gdtype is None:
                 self.gdtype = gd
             elif gd != self.gdtype:
                 raise ValueError("all gradients of one multi-tensor launch must share a dtype")
-            self.arr[i] = TensorDesc(_dev_ptr(p, torch.float32, "p"), _dev_ptr(g, None, "g"),
-                                     _dev_ptr(s1, torch.uint8, "s1"), _dev_ptr(s2, torch.uint8, "s2"),
-                                     _dev_ptr(a1, torch.float32, "absmax1"), _dev_ptr(a2, torch.float32, "absmax2"), n)
-        self.device = entries[0][0].device if entries else None
+            self.arr[i] = TensorDesc(_dev_ptr(p, torch.float32, f"tensor {i} p", dev), _dev_ptr(g, None, f"tensor {i} g", dev),
+                                     _dev_ptr(s1, torch.uint8, f"tensor {i} s1", dev),
+                                     _dev_ptr(s2, torch.uint8, f"tensor {i} s2", dev),
+                                     _dev_ptr(a1, torch.float32, f"tensor {i} absmax1", dev),
+                                     _dev_ptr(a2, torch.float32, f"tensor {i} absmax2", dev), n)
 
     def update_grads(self, grads):
-        """Re-point the descriptors at this step's gradients (same count, sizes and dtype as
+        """Re-point the descriptors at this step's gradients (same count, sizes, dtype and device as
         before); everything else (parameters, states) is unchanged, so no re-validation."""
         if len(grads) != self.count:
             raise ValueError("gradient count changed")
-        arr, gd = self.arr, self.gdtype
+        arr, gd, dev = self.arr, self.gdtype, self.device
         for i, g in enumerate(grads):
-            if not g.is_cuda or GDTYPES.get(g.dtype) != gd or g.numel() != arr[i].n:
+            if g.device != dev or GDTYPES.get(g.dtype) != gd or g.numel() != arr[i].n:
                 raise ValueError(f"tensor {i}: gradient device/size/dtype changed")
             arr[i].g = g.data_ptr()
         self.grads = grads  # keep this step's gradients alive until the next refresh
@@ -272,13 +314,14 @@ def optim8bit_step_multi(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1e-8,
                          bias_correction=True, step=1, blocksize=BLOCKSIZE, hp: HParams | None = None):
     """One fused 8-bit step over many tensors (one launch per <= 384 tensors)."""
     kind = KINDS.get(kind, kind)
-    tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
+    tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors, kind)
     if tl.count == 0:
         return
     if hp is None:
         hp = hparams(lr, beta1, beta2, eps, weight_decay, bias_correction)
-    _check(lib.q8_optim8bit_step_multi(kind, tl.gdtype, tl.arr, tl.count, blocksize, ctypes.byref(hp), int(step),
-                                       _stream(tl.device)))
+    with _on(tl.device):
+        _check(lib.q8_optim8bit_step_multi(kind, tl.gdtype, tl.arr, tl.count, blocksize, ctypes.byref(hp), int(step),
+                                           _stream(tl.device)))
 
 
 def optim32bit_step_multi(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0,
@@ -288,22 +331,26 @@ def optim32bit_step_multi(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1e-8
     entries = list(tensors)
     if not entries:
         return
+    dev = entries[0][0].device
     arr = (TensorDesc32 * len(entries))()
     gd = None
     for i, (p, g, m, r) in enumerate(entries):
         n = p.numel()
-        if g.numel() != n or m.numel() != n or (r is not None and r.numel() != n):
+        if g.numel() != n or m.numel() != n or (r is not None and r.numel() != n) or \
+                (kind != Q8_MOMENTUM and r is None):
             raise ValueError(f"tensor {i}: size mismatch")
+        if g.dtype not in GDTYPES:
+            raise ValueError(f"tensor {i}: unsupported gradient dtype {g.dtype}")
         if gd is None:
             gd = GDTYPES[g.dtype]
         elif GDTYPES[g.dtype] != gd:
             raise ValueError("all gradients of one launch must share a dtype")
-        arr[i] = TensorDesc32(_dev_ptr(p, torch.float32, "p"), _dev_ptr(g, None, "g"), _dev_ptr(m, torch.float32, "m"),
-                              _dev_ptr(r, torch.float32, "r"), n)
+        arr[i] = TensorDesc32(_dev_ptr(p, torch.float32, "p", dev), _dev_ptr(g, None, "g", dev),
+                              _dev_ptr(m, torch.float32, "m", dev), _dev_ptr(r, torch.float32, "r", dev), n)
     if hp is None:
         hp = hparams(lr, beta1, beta2, eps, weight_decay, bias_correction)
-    _check(lib.q8_optim32bit_step_multi(kind, gd, arr, len(entries), ctypes.byref(hp), int(step),
-                                        _stream(entries[0][0].device)))
+    with _on(dev):
+        _check(lib.q8_optim32bit_step_multi(kind, gd, arr, len(entries), ctypes.byref(hp), int(step), _stream(dev)))
 
 
 def layerwise_workspace_bytes(tensors) -> int:
@@ -321,7 +368,7 @@ def optim8bit_step_layerwise(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1
     ratio).  entries as optim8bit_step_multi (s2/absmax2 None for LARS).  Returns the float32
     per-tensor scales RN(lr * ratio) (a view into the workspace, valid until its next use)."""
     kind = KINDS.get(kind, kind)
-    tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors)
+    tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors, kind)
     if tl.count == 0:
         return torch.empty(0, dtype=torch.float32)
     need = lib.q8_layerwise_workspace_bytes(tl.arr, tl.count)
@@ -331,10 +378,11 @@ def optim8bit_step_layerwise(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1
         workspace = torch.empty(need, dtype=torch.uint8, device=tl.device)
     if hp is None:
         hp = hparams(lr, beta1, beta2, eps, weight_decay, bias_correction)
-    _check(lib.q8_optim8bit_step_layerwise(kind, tl.gdtype, tl.arr, tl.count, blocksize, ctypes.byref(hp),
-                                           float(trust_coefficient), int(step), _dev_ptr(workspace, torch.uint8,
-                                                                                         "workspace"),
-                                           workspace.numel(), _stream(tl.device)))
+    with _on(tl.device):
+        _check(lib.q8_optim8bit_step_layerwise(kind, tl.gdtype, tl.arr, tl.count, blocksize, ctypes.byref(hp),
+                                               float(trust_coefficient), int(step),
+                                               _dev_ptr(workspace, torch.uint8, "workspace", tl.device),
+                                               workspace.numel(), _stream(tl.device)))
     return workspace[:4 * tl.count].view(torch.float32)
 
 
@@ -350,18 +398,21 @@ def optim8bit_step_zero_fused(kind, world, rank, g_ptrs, p_ptrs, sig_ptrs, s1, s
     """Fused ZeRO-1 step over peer memory (q8_optim8bit_step_zero_fused): g_ptrs / p_ptrs /
     sig_ptrs are per-rank device addresses (ints) of the gradient, parameter and signal buffers."""
     kind = KINDS.get(kind, kind)
+    dev = s1.device
     arr = ctypes.c_void_p * world
-    _check(lib.q8_optim8bit_step_zero_fused(kind, GDTYPES[g_dtype], world, rank, arr(*g_ptrs), arr(*p_ptrs),
-                                            arr(*sig_ptrs), _dev_ptr(s1, torch.uint8, "s1"),
-                                            _dev_ptr(s2, torch.uint8, "s2"),
-                                            _dev_ptr(absmax1, torch.float32, "absmax1"),
-                                            _dev_ptr(absmax2, torch.float32, "absmax2"), int(n_pad), BLOCKSIZE,
-                                            ctypes.byref(hp), int(step), int(epoch), int(num_ctas),
-                                            stream if stream is not None else _stream(s1.device)))
+    with _on(dev):
+        _check(lib.q8_optim8bit_step_zero_fused(kind, GDTYPES[g_dtype], world, rank, arr(*g_ptrs), arr(*p_ptrs),
+                                                arr(*sig_ptrs), _dev_ptr(s1, torch.uint8, "s1"),
+                                                _dev_ptr(s2, torch.uint8, "s2", dev),
+                                                _dev_ptr(absmax1, torch.float32, "absmax1", dev),
+                                                _dev_ptr(absmax2, torch.float32, "absmax2", dev), int(n_pad),
+                                                BLOCKSIZE, ctypes.byref(hp), int(step), int(epoch), int(num_ctas),
+                                                stream if stream is not None else _stream(dev)))
 
 
-def quantiles_workspace_bytes(n: int) -> int:
-    nb = lib.q8_quantiles_workspace_bytes(int(n))
+def quantiles_workspace_bytes(n: int, device=None) -> int:
+    with _on(device if device is not None else torch.cuda.current_device()):
+        nb = lib.q8_quantiles_workspace_bytes(int(n))
     if nb < 0:
         raise Q8Error(Q8_ERR_INVALID, lib.q8_last_error().decode() or "invalid n")
     return nb
@@ -372,20 +423,22 @@ def estimate_quantiles(x: torch.Tensor, *, with_codebook: bool = False, workspac
     """SRAM-Quantiles (App G): the 257 quantiles Q(j/257) of x (fp32, on the GPU).  With
     with_codebook, also the Eq.5 quantile data type (256 fp32 in [-1, 1], on the GPU), usable
     as the `code` table of quantize_blockwise.  Returns quantiles or (quantiles, code)."""
-    n = x.numel()
-    need = quantiles_workspace_bytes(n)
+    n, dev = x.numel(), x.device
+    need = quantiles_workspace_bytes(n, dev)
     if workspace is None or workspace.numel() < need:
-        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
     if quantiles is None:
-        quantiles = torch.empty(257, dtype=torch.float32, device=x.device)
+        quantiles = torch.empty(257, dtype=torch.float32, device=dev)
     if with_codebook and code is None:
-        code = torch.empty(256, dtype=torch.float32, device=x.device)
+        code = torch.empty(256, dtype=torch.float32, device=dev)
     if quantiles.numel() != 257 or (code is not None and code.numel() != 256):
         raise ValueError("size mismatch")
-    _check(lib.q8_estimate_quantiles(_dev_ptr(x, torch.float32, "x"), n, _dev_ptr(quantiles, torch.float32, "quantiles"),
-                                     _dev_ptr(code, torch.float32, "code") if with_codebook else None,
-                                     _dev_ptr(workspace, torch.uint8, "workspace"), workspace.numel(),
-                                     _stream(x.device)))
+    with _on(dev):
+        _check(lib.q8_estimate_quantiles(_dev_ptr(x, torch.float32, "x"), n,
+                                         _dev_ptr(quantiles, torch.float32, "quantiles", dev),
+                                         _dev_ptr(code, torch.float32, "code", dev) if with_codebook else None,
+                                         _dev_ptr(workspace, torch.uint8, "workspace", dev), workspace.numel(),
+                                         _stream(dev)))
     return (quantiles, code) if with_codebook else quantiles
 
 
@@ -404,8 +457,10 @@ def count_nonfinite(g: torch.Tensor, out: torch.Tensor | None = None) -> torch.T
     sync): the AMP-style guard before an 8-bit step (non-finite gradients are out of contract)."""
     if g.dtype not in GDTYPES:
         raise ValueError(f"unsupported gradient dtype {g.dtype}")
+    dev = g.device
     if out is None:
-        out = torch.empty(1, dtype=torch.int64, device=g.device)
-    _check(lib.q8_count_nonfinite(_dev_ptr(g, None, "g"), GDTYPES[g.dtype], g.numel(),
-                                  _dev_ptr(out, torch.int64, "out"), _stream(g.device)))
+        out = torch.empty(1, dtype=torch.int64, device=dev)
+    with _on(dev):
+        _check(lib.q8_count_nonfinite(_dev_ptr(g, None, "g"), GDTYPES[g.dtype], g.numel(),
+                                      _dev_ptr(out, torch.int64, "out", dev), _stream(dev)))
     return out

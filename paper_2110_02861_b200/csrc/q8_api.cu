@@ -207,8 +207,15 @@ int nsub_variant(q8_dtype gdt) {
     return env ? std::min(env, mx) : mx;
 }
 
+// Kernels already opted into their dynamic shared memory, per device (the attribute is set
+// per device: a process stepping tensors on two GPUs needs it on both).
 std::mutex g_smem_mu;
-const void* g_smem_done[256];
+struct SmemDone {
+    int dev;
+    const void* fn;
+};
+SmemDone g_smem_done[1024];
+int g_smem_count = 0;
 
 template <int MAXT>
 q8_status dispatch_step(q8_kind kind, q8_dtype gdt, const q8::StepParams<MAXT>& P, const DeviceState* d,
@@ -242,13 +249,16 @@ q8_status check_common(q8_dtype gdt, int32_t blocksize) {
 }  // namespace
 
 cudaError_t q8::ensure_smem(const void* fn, int smem) {
-    std::lock_guard<std::mutex> lock(g_smem_mu);
-    for (const void* c : g_smem_done)
-        if (c == fn) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    for (auto& c : g_smem_done)
-        if (!c) { c = fn; break; }
+    std::lock_guard<std::mutex> lock(g_smem_mu);
+    for (int i = 0; i < g_smem_count; ++i)
+        if (g_smem_done[i].fn == fn && g_smem_done[i].dev == dev) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    if (g_smem_count < static_cast<int>(sizeof g_smem_done / sizeof g_smem_done[0]))
+        g_smem_done[g_smem_count++] = SmemDone{dev, fn};
     return cudaSuccess;
 }
 
@@ -261,9 +271,10 @@ const char* q8_version(void) { return "q8 0.1 sm_100a"; }
 q8_status q8_create_linear_codebook(int32_t is_signed, float* out_host) {
     if (!out_host) return fail(Q8_ERR_INVALID, "out_host is NULL");
     for (int i = 0; i < 256; ++i) {
-        // 256 evenly spaced values over [-1, 1] (signed) or [0, 1] (unsigned), each computed in
-        // double and rounded once (linear quantization, T3 caption P:214)
-        const double v = is_signed ? -1.0 + 2.0 * static_cast<double>(i) / 255.0 : static_cast<double>(i) / 255.0;
+        // linear quantization (T3 caption P:214), reading L0: signed (i - 127)/128 -- even spacing
+        // 1/128, exact 0 at index 127 and +1 at 255 (the dynamic type's layout of its specials);
+        // unsigned i/255.  Computed in double and rounded once (both are exact in binary32).
+        const double v = is_signed ? static_cast<double>(i - 127) / 128.0 : static_cast<double>(i) / 255.0;
         out_host[i] = static_cast<float>(v);
     }
     return ok();
@@ -271,11 +282,15 @@ q8_status q8_create_linear_codebook(int32_t is_signed, float* out_host) {
 
 // ---------------------------------------------------------------- SRAM-Quantiles (App G)
 namespace {
+// Resident CTAs per SM are cached process-wide: the library runs only on sm_100a devices, whose
+// SMs have identical register files and shared memory, so the occupancy of a kernel is the same on
+// every device; the shared-memory opt-in itself is per device (ensure_smem).
 int quantile_rows(const DeviceState* d, int64_t nchunks) {
+    if (q8::ensure_smem(reinterpret_cast<const void*>(q8::sram_quantiles_kernel), q8::kQSmemBytes) != cudaSuccess)
+        return 1;
     static int occ = [] {
         int o = 0;
-        if (q8::ensure_smem(reinterpret_cast<const void*>(q8::sram_quantiles_kernel), q8::kQSmemBytes) != cudaSuccess ||
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, q8::sram_quantiles_kernel, q8::kQThreads,
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, q8::sram_quantiles_kernel, q8::kQThreads,
                                                           q8::kQSmemBytes) != cudaSuccess || o < 1)
             o = 1;
         const char* env = std::getenv("Q8_QUANTILE_CTAS_PER_SM");

@@ -56,13 +56,16 @@ class _Optimizer8bit(torch.optim.Optimizer):
         return st
 
     def _tensor_list(self, group, gdt, entries):
-        """The multi-tensor descriptor array for these entries, cached per (group, dtype, parameter
-        storage): a parameter whose .data is re-pointed gets a new key; states only change storage in
-        load_state_dict, which clears the cache; gradients (re-allocated by backward) are refreshed."""
-        key = (id(group), gdt, tuple(e[0].data_ptr() for e in entries))
+        """The multi-tensor descriptor array for these entries, cached per (group, dtype, parameter and
+        state storage): a parameter whose .data is re-pointed, or a state that was reset or replaced
+        (opt.state.clear(), load_state_dict, new s1/absmax tensors), gets a new key; gradients
+        (re-allocated by backward) are refreshed in place."""
+        key = (id(group), gdt, tuple((e[0].data_ptr(), e[2].data_ptr(), e[4].data_ptr(),
+                                      e[3].data_ptr() if e[3] is not None else 0,
+                                      e[5].data_ptr() if e[5] is not None else 0) for e in entries))
         tl = self._lists.get(key)
         if tl is None:
-            tl = B.TensorList(entries)
+            tl = B.TensorList(entries, self.kind)
             if len(self._lists) > 64:
                 self._lists.clear()
             self._lists[key] = tl

@@ -315,3 +315,24 @@ def test_tensorwise_codec_bit_exact(q8, n, table):
     assert_same(a_g, a_r, "absmax")
     assert_same(c_g, c_r, "codes")
     assert_same(q8.dequantize_tensorwise(code_dev, c_g, a_g), oracle.dequantize_blockwise(Q, c_r, a_r, n), "deq")
+
+
+@pytest.mark.parametrize("signed", [True, False])
+def test_linear_type_zero_round_trip(q8, signed):
+    """Reading L0: exact zeros in a block with a nonzero absmax come back as exact zeros through the
+    linear type (block-wise and tensor-wise codecs), identically to the oracle."""
+    n = 3 * 2048 + 77
+    Q = oracle.linear_codebook(signed)
+    x = synth.params(n, seed=41, std=1.0)
+    if not signed:
+        x = x.abs()
+    x[::3] = 0.0
+    code_dev = torch.from_numpy(Q).to(DEV)
+    a_g, c_g = q8.quantize_blockwise(code_dev, x.to(DEV))
+    a_r, c_r = oracle.quantize_blockwise(Q, x.numpy())
+    assert_same(a_g, a_r, "absmax")
+    assert_same(c_g, c_r, "codes")
+    d = q8.dequantize_blockwise(code_dev, c_g, a_g).cpu()
+    assert torch.all(d[::3] == 0.0) and torch.all(c_g.cpu()[::3] == (127 if signed else 0))
+    a_t, c_t = q8.quantize_tensorwise(code_dev, x.to(DEV))
+    assert torch.all(q8.dequantize_tensorwise(code_dev, c_t, a_t).cpu()[::3] == 0.0)

@@ -108,13 +108,16 @@ def test_every_code_round_trips(signed):
 
 @pytest.mark.parametrize("signed", [True, False])
 def test_linear_codebook(signed):
-    """Linear type (T3 caption): 256 evenly spaced values with exact endpoints."""
+    """Linear type (T3 caption; reading L0): 256 evenly spaced values, max +1, an exact 0
+    (zero-initialized states must round-trip, Eq.2), the signed type symmetric apart from +1."""
     Q = oracle.linear_codebook(signed).astype(np.float64)
     assert Q.size == 256 and np.all(np.diff(Q) > 0)
-    assert Q[-1] == 1.0 and Q[0] == (-1.0 if signed else 0.0)
+    assert Q[-1] == 1.0 and Q[0] == (-127 / 128 if signed else 0.0)
     step = (Q[-1] - Q[0]) / 255
     assert np.max(np.abs(np.diff(Q) - step)) <= 2 * np.spacing(np.float32(1.0))   # even spacing
+    assert Q[127 if signed else 0] == 0.0                                            # exact zero
     if signed:
-        assert np.array_equal(Q, -Q[::-1])                                           # symmetric
+        assert np.array_equal(Q[:255], -Q[:255][::-1])                              # symmetric but +1
+        assert step == 1 / 128
     assert np.array_equal(oracle.nearest_code(oracle.linear_codebook(signed), oracle.linear_codebook(signed)),
                           np.arange(256, dtype=np.uint8))

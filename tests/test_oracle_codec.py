@@ -123,3 +123,18 @@ def test_idempotence_positive_max_blocks(Qs):
     a, c = oracle.quantize_blockwise(Qs, x, 2048)
     a2, c2 = oracle.quantize_blockwise(Qs, oracle.dequantize_blockwise(Qs, c, a, 2048), 2048)
     assert np.array_equal(c, c2) and np.array_equal(a, a2)
+
+
+@pytest.mark.parametrize("signed", [True, False])
+def test_linear_type_keeps_exact_zeros(signed):
+    """Reading L0: a zero element of a block with a nonzero absmax decodes to exactly 0 through the
+    linear type (with the rejected symmetric -1 + 2i/255 grid it would decode to +-N/255)."""
+    Q = oracle.linear_codebook(signed)
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(5000).astype(np.float32)
+    if not signed:
+        x = np.abs(x)
+    x[::4] = 0.0
+    absmax, codes = oracle.quantize_blockwise(Q, x)
+    d = oracle.dequantize_blockwise(Q, codes, absmax, x.size)
+    assert np.all(d[::4] == 0.0) and np.all(absmax > 0)
