@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--zero1-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--oracle-timings", action="store_true",
+                    help="also time the oracle single-threaded (SURVEY 8(d-6); default for cfg2)")
     ap.add_argument("--force-zero1", action="store_true", help="run the ZeRO-1 round trip even at one rank")
     ap.add_argument("--zero-fused", action="store_true",
                     help="also time the fused ZeRO-1 kernel (peer-memory RS + step + AG in one launch)")
@@ -181,6 +183,37 @@ def oracle_sample(cfg, target_s: float = 10.0):
                              f"{1e9 * dt2 / n2:.2f} ns/param")
 
 
+def oracle_timing_set(cfg):
+    """the oracle on this host, as it stands -- one thread on config 1 (2^20 elements,
+    Adam, fp32 grads), one thread on a 2^26-element slice of the workload, and every host core on
+    the whole workload buffer (capped at the cfg2 size, 354,823,168 parameters).  ns/param and
+    params/s per leg; the core count is the host's (never hard-coded)."""
+    import oracle
+    cores = os.cpu_count() or 1
+    kind, gdt = cfg["kind"], cfg["grad_dtype"]
+    hp = dict(cfg["hparams"])
+    legs = []
+
+    def leg(name, n, k, g_dt, hpar, threads):
+        p = synth.params(n, seed=21).numpy()
+        g = synth.to_f32_numpy(synth.grads(n, step=2, seed=21, dtype=g_dt))
+        s1, a1 = (t.numpy() for t in synth.random_state(n, seed=22, scale=1e-3))
+        s2, a2 = (t.numpy() for t in synth.random_state(n, seed=23, scale=1e-6))
+        t0 = time.perf_counter()
+        oracle.optim8bit_step(k, p, g, s1, s2, a1, a2, step=2, nthreads=threads, **hpar)
+        dt = time.perf_counter() - t0
+        legs.append({"leg": name, "n_params": n, "threads": threads, "kind": k, "s": dt,
+                     "ns_per_param": 1e9 * dt / n, "params_per_s": n / dt})
+
+    leg("cfg1 (2^20 elements), 1 thread", 1 << 20, "adam", "float32", synth.HPARAMS["adam"], 1)
+    leg(f"2^26-element slice of {cfg['workload'].split(':')[0]}, 1 thread", 1 << 26, kind, gdt, hp, 1)
+    n_all = min(cfg["n_params"], 354_823_168)
+    leg(f"{n_all:,} parameters of {cfg['workload'].split(':')[0]}, {cores} threads", n_all, kind, gdt, hp, cores)
+    return {"legs": legs, "cores": cores, "cpu": cpu_model(),
+            "paper_context": "T5 (P:358-365, V100, 32-bit grads): 8-bit Adam 47 ms, 8-bit Momentum 34 ms per "
+                             "update of 1B parameters"}
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -251,11 +284,24 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    # More ranks than visible GPUs (e.g. torchrun --nproc-per-node 4 on a one-GPU box): the ranks
+    # share the GPUs.  NCCL refuses two ranks on one device ("Duplicate GPU detected"), so the host
+    # exchange goes over gloo and the data plane is the fused ZeRO-1 kernel over CUDA IPC peer
+    # memory (main_shared).
+    ndev = torch.cuda.device_count()
+    shared = world > 1 and ndev < world
+    if shared:
+        local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1 or "RANK" in os.environ:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = workload_config(args.workload, world)
+    if shared:
+        return main_shared(args, cfg, q8, zero, world, rank, local, dev)
     if synth.WORKLOADS[args.workload].get("layerwise"):
         return main_layerwise(args, cfg, q8, world, rank, local, dev)
     if synth.WORKLOADS[args.workload].get("multi"):
@@ -264,6 +310,8 @@ def main():
         return main_optim_api(args, cfg, q8, world, rank, local, dev)
     if synth.WORKLOADS[args.workload].get("quantiles"):
         return main_quantiles(args, cfg, q8, world, rank, local, dev)
+    if synth.WORKLOADS[args.workload].get("codec"):
+        return main_codec(args, cfg, q8, world, rank, local, dev)
     kind, gdt = cfg["kind"], cfg["grad_dtype"]
     hp = dict(cfg["hparams"])
     n_total = cfg["n_params"]
@@ -297,6 +345,14 @@ def main():
     torch.cuda.synchronize()
     # state realism check: the most common code should hold < 5% of elements
     share1 = float(torch.bincount(s1[:1 << 24].to(torch.int64), minlength=256).max()) / min(shard, 1 << 24)
+    share2 = (float(torch.bincount(s2[:1 << 24].to(torch.int64), minlength=256).max()) / min(shard, 1 << 24)
+              if kind not in ("momentum", "lars") else None)
+    realism = {"s1_most_common_code_share": share1, "s2_most_common_code_share": share2,
+               "s1_distinct_codes": int((torch.bincount(s1[:1 << 24].to(torch.int64), minlength=256) > 0).sum()),
+               "s2_distinct_codes": (int((torch.bincount(s2[:1 << 24].to(torch.int64), minlength=256) > 0).sum())
+                                     if share2 is not None else None),
+               "bar": "most common code < 5% of elements per state (SURVEY 8(d-5)); first 2^24 elements",
+               "ok": share1 < 0.05 and (share2 is None or share2 < 0.05)}
 
     stream = torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -505,18 +561,24 @@ def main():
             torch.cuda.empty_cache()
 
     cpu_baseline = None
+    oracle_timings = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, cores, sample = oracle_sample(cfg)
         cpu_baseline = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        if args.oracle_timings or args.workload == "cfg2_gpt2_medium":
+            oracle_timings = oracle_timing_set(cfg)
 
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic: p~N(0,0.02^2), bf16 g~N(0,1e-3^2) (pool of 2), 8-bit states evolved from zero "
-                    f"over the warm-up; most common s1 code after warm-up holds {100 * share1:.1f}% of elements",
-            "config": cfg, "roofline": roofline, "cpu_baseline": cpu_baseline, "e2e": e2e,
+            "data": f"synthetic: p~N(0,0.02^2), {gdt} g~N(0,1e-3^2) (pool of 2), 8-bit states evolved from zero "
+                    f"over the warm-up; most common code after warm-up holds {100 * share1:.1f}% (s1)"
+                    + (f" / {100 * share2:.1f}% (s2)" if share2 is not None else "") + " of elements",
+            "state_realism": realism,
+            "config": cfg, "roofline": roofline, "cpu_baseline": cpu_baseline, "oracle_timings": oracle_timings,
+            "e2e": e2e,
             "e2e_resident_states": e2e_res, "zero1": zero1,
             "gpu_launches": args.steps, "clocks": clk.summary(),
             "achieved_gbs_whole_job": n_total * bpp / (ms_per_step / 1e3) / 1e9,
@@ -557,6 +619,137 @@ def zero1_check(zo, q8, kind, hp):
     flag = torch.tensor([0 if ok else 1], dtype=torch.int32, device=zo.params.device)
     dist.all_reduce(flag, op=dist.ReduceOp.MAX)
     return "bit-exact vs the unsharded step on the reduced gradient" if int(flag[0]) == 0 else "MISMATCH"
+
+
+def zero_fused_check(zf, q8, kind, hp, gdt):
+    """Bit-exactness of one more fused ZeRO-1 step (SURVEY 8(e) procedure, reading Z1): the shard
+    gradient is the rank-order binary32 sum of every rank's gradient divided by the world size, so
+    rank 0 rebuilds it from the peers' buffers (CUDA IPC mappings) with tensor operations (IEEE adds
+    in rank order, IEEE division by a tensor), gathers every rank's initial shard states the same
+    way, runs the UNSHARDED single-GPU step on the whole buffer and compares parameters (every
+    rank's replica), codes and absmax bit for bit.  The verdict is broadcast to all ranks."""
+    from paper_2110_02861_b200 import zero
+    world, rank = zf.world, zf.rank
+    names = ["s1", "absmax1"] + (["s2", "absmax2"] if zf.s2 is not None else [])
+    mine = [getattr(zf, k) for k in names]
+    peers = zero.exchange_peer_tensors(mine) if world > 1 else [mine]
+    torch.cuda.synchronize()
+    dist.barrier()
+    ok = True
+    if rank == 0:
+        st0 = [torch.cat([peers[r][i] for r in range(world)]).clone() for i in range(len(names))]
+        p_ref = zf.params.clone()
+    zf.grads.zero_()
+    zf.grads[:zf.n] = synth.grads(zf.n, step=77, seed=100 + rank, dtype=gdt, device=zf.grads.device)
+    torch.cuda.synchronize()
+    dist.barrier()
+    if rank == 0:
+        gsrc = [zf._peers[r][0] for r in range(world)]
+        acc = gsrc[0].to(torch.float32)
+        for r in range(1, world):
+            acc = acc + gsrc[r].to(torch.float32)          # binary32 adds in rank order (Z1)
+        acc = acc / torch.full_like(acc, float(world))     # IEEE division (tensor divisor)
+        torch.cuda.synchronize()
+    dist.barrier()
+    zf.step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    if rank == 0:
+        s1r, a1r = st0[0], st0[1]
+        s2r, a2r = (st0[2], st0[3]) if len(st0) > 2 else (None, None)
+        q8.optim8bit_step(kind, p_ref, acc, s1r, s2r, a1r, a2r, step=zf.t, lr=hp["lr"],
+                          **{k: v for k, v in hp.items() if k != "lr"})
+        torch.cuda.synchronize()
+        for r in range(world):
+            pr = zf._peers[r][1]
+            ok = ok and torch.equal(pr.view(torch.int32), p_ref.view(torch.int32))
+        new = [torch.cat([peers[r][i] for r in range(world)]) for i in range(len(names))]
+        ref = [s1r, a1r] + ([s2r, a2r] if s2r is not None else [])
+        for a, b in zip(new, ref):
+            ok = ok and torch.equal(a.view(torch.uint8), b.view(torch.uint8))
+    flag = torch.tensor([0 if ok else 1], dtype=torch.int32)
+    dist.broadcast(flag, 0)
+    dist.barrier()
+    return ("bit-exact vs the unsharded step on the rank-order reduced gradient (all replicas, codes, absmax)"
+            if int(flag[0]) == 0 else "MISMATCH")
+
+
+def main_shared(args, cfg, q8, zero_mod, world, rank, local, dev):
+    """Ranks sharing one GPU (world > visible GPUs): the data plane is the fused ZeRO-1 kernel
+    (q8_optim8bit_step_zero_fused: every rank reduces its shard's gradient from every rank's buffer
+    over CUDA IPC peer memory, steps the shard and writes the new parameters into every rank's
+    replica, one launch per rank per step); gloo carries only the host exchange (IPC handles,
+    barriers, max-over-ranks timing).  Without MPS the ranks' kernels time-slice the one GPU, so
+    the throughput is not a scaling number: this mode proves the multi-rank path bit-exact
+    (zero_fused_check) and gives the N-rank JSON line."""
+    kind, gdt = cfg["kind"], cfg["grad_dtype"]
+    hp = dict(cfg["hparams"])
+    n_total = cfg["n_params"]
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    ctas = max(1, sms // world)
+    zf = zero_mod.ZeroFusedOptimizer8bit(n_total, kind=kind, grad_dtype=TORCH_DT[gdt], device=dev, num_ctas=ctas,
+                                         **hp)
+    zf.params[:n_total] = synth.params(n_total, seed=1, device=dev)  # identical replicas on every rank
+    gpool = [synth.grads(n_total, step=t, seed=rank, dtype=gdt, device=dev) for t in (1, 2)]
+    torch.cuda.synchronize()
+    dist.barrier()
+
+    def one(i):
+        zf.grads[:n_total].copy_(gpool[i % 2])
+        zf.step()
+
+    for i in range(args.warmup):
+        one(i)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stream = torch.cuda.current_stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for i in range(args.steps):
+            zf.grads[:n_total].copy_(gpool[i % 2])   # a new gradient per step (outside the kernel events)
+            ev[i][0].record(stream)
+            zf.step()
+            ev[i][1].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([t0.elapsed_time(t1) / args.steps, statistics.mean(a.elapsed_time(b) for a, b in ev)],
+                      dtype=torch.float64)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_per_step, kern_ms = float(ms[0]), float(ms[1])
+    check = zero_fused_check(zf, q8, kind, hp, gdt)
+    bpp = bytes_per_param(kind, gdt)
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs", 6650.0)
+    # HBM bytes of one step of the whole job: each rank reads its shard's gradient from all W
+    # buffers and writes its new shard parameters into all W replicas (plus p read, states r/w)
+    gb = 4 if gdt == "float32" else 2
+    bpp_fused = bpp + (world - 1) * (gb + 4)
+    achieved = zf.n_pad * bpp_fused / (kern_ms / 1e3) / 1e9
+    if rank == 0:
+        cfg = dict(cfg, parallelism=f"zero1-fused-dp{world} (ranks share {torch.cuda.device_count()} GPU: "
+                                    f"gloo host exchange, CUDA IPC data plane, {ctas} CTAs per rank)")
+        print(json.dumps({
+            "metric": METRIC, "value": n_total / (ms_per_step / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": f"synthetic: p~N(0,0.02^2), {gdt} g~N(0,1e-3^2) per rank (pool of 2), states evolved from zero",
+            "config": cfg,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "bytes_per_param": bpp_fused, "algorithmic_bytes_per_launch": None,
+                         "kernel": "optim8bit_step_kernel MODE_ZERO (W ranks' launches on one GPU, time-sliced)",
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
+                         else "fallback 6.65 TB/s (B200_PROFILING.md)"},
+            "shared_gpu": {"ranks_per_gpu": world, "note": "without MPS the W processes' kernels time-slice one "
+                           "GPU: a correctness mode of the multi-rank data plane, not a scaling measurement"},
+            "zero1": {"fused": {"ms_per_step": ms_per_step, "kernel_ms": kern_ms, "check": check,
+                                "backend": "gloo (host) + CUDA IPC peer memory (data)"}},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": args.steps, "clocks": clk.summary(),
+            "library": q8.version(),
+        }))
+    dist.destroy_process_group()
 
 
 def main_layerwise(args, cfg, q8, world, rank, local, dev):
@@ -824,10 +1017,39 @@ def main_optim_api(args, cfg, q8, world, rank, local, dev):
             host.append(time.perf_counter() - t0)
             ev[i][1].record(stream)
         torch.cuda.synchronize()
-    ms = torch.tensor([statistics.mean(a.elapsed_time(b) for a, b in ev)], dtype=torch.float64, device=dev)
+    # the same step through a CUDA graph: AdamW8bit(capturable=True) keeps the step counter on the
+    # device (q8_plan_step_device), so step() is captured once and replayed with no host work
+    del opt
+    torch.cuda.empty_cache()
+    gopt = q8.AdamW8bit(params, lr=hp["lr"], betas=(hp["beta1"], hp["beta2"]), eps=hp["eps"],
+                        weight_decay=hp["weight_decay"], capturable=True)
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(side):
+        for _ in range(max(1, args.warmup)):
+            gopt.step()
+    torch.cuda.current_stream(dev).wait_stream(side)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        gopt.step()
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ghost = []
+    for i in range(args.steps):
+        gev[i][0].record(stream)
+        t0 = time.perf_counter()
+        graph.replay()
+        ghost.append(time.perf_counter() - t0)
+        gev[i][1].record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([statistics.mean(a.elapsed_time(b) for a, b in ev),
+                       statistics.mean(a.elapsed_time(b) for a, b in gev)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms_per_step = float(ms[0])
+    ms_per_step, ms_graph = float(ms[0]), float(ms[1])
     n_total = sum(synth.numel(sh) for sh in shapes)
     bpp = bytes_per_param(kind, gdt)
     peaks = measured_peaks()
@@ -844,11 +1066,109 @@ def main_optim_api(args, cfg, q8, world, rank, local, dev):
             "config": cfg,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": None, "bytes_per_param": bpp, "algorithmic_bytes_per_launch": n_total * bpp,
-                         "kernel": "optim8bit_step_kernel (multi-tensor, 2 launches for 580 tensors)",
+                         "kernel": "optim8bit_step_kernel (plan launch, 2 launches for 580 tensors)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
                          else "fallback 6.65 TB/s (B200_PROFILING.md)"},
             "host_ms_per_step": 1e3 * statistics.median(host),
+            "eager": {"ms_per_step": ms_per_step, "host_ms_per_step": 1e3 * statistics.median(host),
+                      "path": "AdamW8bit.step(): cached plan (q8_plan_step), gradient pointers refreshed per step"},
+            "cuda_graph": {"ms_per_step": ms_graph, "host_ms_per_step": 1e3 * statistics.median(ghost),
+                           "value": world * n_total / (ms_graph / 1e3),
+                           "path": "AdamW8bit(capturable=True).step() captured once in a CUDA graph, "
+                                   "graph.replay() per step (device step counter, q8_plan_step_device)"},
             "cpu_baseline": None, "e2e": None, "gpu_launches": args.steps * ((len(shapes) + 383) // 384),
+            "clocks": clk.summary(), "library": q8.version(),
+        }))
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+def main_codec(args, cfg, q8, world, rank, local, dev):
+    """The stand-alone block-wise codec (Eq.4): one step = quantize a
+    GPT-2-XL-sized fp32 buffer with the built-in signed dynamic type (q8_quantize_blockwise_dynamic:
+    the step kernel's bucketed search), quantize it with the same type passed as a caller table
+    (q8_quantize_blockwise: Eytzinger 8-step search, thresholds derived per CTA), and dequantize
+    (q8_dequantize_blockwise).  Algorithmic bytes per element: 4 (x) + 1 (code) + 4/2048 (absmax)
+    each way; each kernel is timed on its own with CUDA events.  Independent
+    problems per GPU (replicas)."""
+    n = cfg["n_params"]
+    x = synth.params(n, seed=1 + rank, device=dev)
+    code = q8.create_dynamic_codebook(True).to(dev)
+    nb = (n + 2047) // 2048
+    a_dyn = torch.empty(nb, dtype=torch.float32, device=dev)
+    c_dyn = torch.empty(n, dtype=torch.uint8, device=dev)
+    a_gen = torch.empty(nb, dtype=torch.float32, device=dev)
+    c_gen = torch.empty(n, dtype=torch.uint8, device=dev)
+    out = torch.empty(n, dtype=torch.float32, device=dev)
+    ops = {"quantize_dynamic": lambda: q8.quantize_blockwise_dynamic(True, x, a_dyn, c_dyn),
+           "quantize_generic": lambda: q8.quantize_blockwise(code, x, a_gen, c_gen),
+           "dequantize": lambda: q8.dequantize_blockwise(code, c_dyn, a_dyn, out)}
+    for _ in range(args.warmup):
+        for f in ops.values():
+            f()
+    torch.cuda.synchronize()
+    same = bool(torch.equal(c_dyn, c_gen) and torch.equal(a_dyn, a_gen))
+    stream = torch.cuda.current_stream()
+    ev = {k: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+          for k in ops}
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for i in range(args.steps):
+            for k, f in ops.items():
+                ev[k][i][0].record(stream)
+                f()
+                ev[k][i][1].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms = torch.tensor([t0.elapsed_time(t1) / args.steps] + [statistics.mean(a.elapsed_time(b) for a, b in ev[k])
+                                                             for k in ops], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_step = float(ms[0])
+    per = {k: float(v) for k, v in zip(ops, ms[1:])}
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs", 6650.0)
+    bpe = 4 + 1 + 4 / 2048
+    kern = {k: {"ms": v, "elements_per_s": n / (v / 1e3), "achieved_gbs": n * bpe / (v / 1e3) / 1e9,
+                "frac": n * bpe / (v / 1e3) / 1e9 / peak} for k, v in per.items()}
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if world == 1 and os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        m = 1 << 26
+        xs = x[:m].cpu().numpy()
+        Q = oracle.dynamic_codebook(True)
+        tq = time.perf_counter()
+        oracle.quantize_blockwise(Q, xs)
+        dt = time.perf_counter() - tq
+        cpu_baseline = {"value": m / dt, "unit": "elements/s", "cores": 1, "kind": "oracle",
+                        "sample": f"oracle.quantize_blockwise over the first {m:,} elements, 1 thread, {dt:.1f} s"}
+    if rank == 0:
+        k0 = kern["quantize_dynamic"]
+        cfg = {"workload": cfg["workload"], "n_elements": n, "blocksize": 2048, "table": "signed dynamic tree",
+               "parallelism": f"replicas-{world}" if world > 1 else "single-gpu",
+               "l2": "inputs (6.2 GB) exceed the 126 MB L2; no flush between steps"}
+        print(json.dumps({
+            "metric": "block-wise quantize + dequantize elements/sec (Eq.4 codec, SURVEY 8(a) a8)",
+            "value": world * n / (ms_step / 1e3), "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic: x ~ N(0, 0.02^2) fp32", "config": cfg,
+            "roofline": {"bound": "hbm", "achieved": k0["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                         "frac": k0["frac"], "traffic": traffic, "bytes_per_element": bpe,
+                         "algorithmic_bytes_per_launch": n * bpe,
+                         "kernel": "quantize_blockwise_dynamic_kernel (the dominant launch of the step)",
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
+                         else "fallback 6.65 TB/s (B200_PROFILING.md)"},
+            "kernels": kern, "dynamic_equals_generic": same,
+            "cpu_baseline": cpu_baseline, "e2e": None, "gpu_launches": args.steps * 3,
             "clocks": clk.summary(), "library": q8.version(),
         }))
     if dist.is_initialized():

@@ -255,9 +255,13 @@ int64_t q8_layerwise_workspace_bytes(const q8_tensor* tensors_host, int32_t num_
  * every rank's pad and waits for all ranks' flags before reading gradients, and again after its
  * parameter writes; so when the call completes on `stream`, every rank's gradients have been
  * consumed and this rank's parameter buffer holds all shards.  epoch must start at 1 and grow by
- * one per call (the pads are never reset); every rank must make the same sequence of calls with
- * the same num_ctas (0 = one CTA per SM; all ranks' CTAs must be co-resident: on a shared GPU use
- * num_ctas <= SMs / world).  A rank that never arrives makes the kernel trap after ~30 s.
+ * one per call (the pads are never reset).  Launch contract: every rank makes the same sequence of
+ * calls with the same num_ctas (0 = one CTA per SM).  The grid is launched cooperatively, so the
+ * runtime guarantees that all of this rank's CTAs are resident at once (CUDA error
+ * "cooperative launch too large" otherwise) -- with one rank per GPU that is sufficient for
+ * progress.  Ranks sharing one GPU under MPS must also fit together (num_ctas <= SMs / world);
+ * without MPS their kernels time-slice and still make progress.  A rank that never arrives (a
+ * crashed peer) makes the kernel trap after ~30 s instead of hanging the GPU.
  * world <= 16.  Errors: as q8_optim8bit_step, plus INVALID for bad world/rank/n_pad/epoch/num_ctas. */
 q8_status q8_optim8bit_step_zero_fused(q8_kind kind, q8_dtype g_dtype, int32_t world, int32_t rank,
                                        const void* const* g_peers_host, float* const* p_peers_host,
@@ -276,6 +280,55 @@ int64_t q8_zero_signal_bytes(int32_t world, int32_t num_ctas);
  *   count_dev  one uint64 on the device, 8-B aligned (written: zeroed then accumulated on stream)
  * Errors: INVALID for n < 0, NULL, misalignment or a bad dtype. */
 q8_status q8_count_nonfinite(const void* g_dev, q8_dtype g_dtype, int64_t n, uint64_t* count_dev, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Prepared multi-tensor steps ("plans"): the paper's drop-in optimizer ("changing two lines of
+ * code") steps the same parameter list every iteration, so the descriptor arrays of
+ * q8_optim8bit_step_multi are built and validated once, kept by the library, and each step costs
+ * one host call (plus, when backward re-allocates gradients, one q8_plan_set_grads).  A plan may mix
+ * 8-bit-state tensors with 32-bit-state tensors (the Stable Embedding layer, "the only layer that
+ * uses 32-bit optimizer states", S3.3 P:124-125): both are stepped by the SAME kernel launch.
+ * ------------------------------------------------------------------------------------------- */
+typedef struct q8_plan q8_plan;
+
+/* Build a plan for kind (Q8_ADAM, Q8_ADAMW or Q8_MOMENTUM) over t8[n8] (8-bit states, as
+ * q8_optim8bit_step_multi) and t32[n32] (32-bit states, as q8_optim32bit_step_multi); tensor k of
+ * the plan is t8[k] for k < n8 and t32[k - n8] after that.  All buffers live on the current
+ * device, which the plan remembers; the library copies the descriptors (caller keeps ownership
+ * of every buffer and must keep them alive while the plan is used).  *out receives the plan.
+ * Errors: as q8_optim8bit_step_multi / q8_optim32bit_step_multi; CUDA if the plan's device
+ * counter cannot be allocated. */
+q8_status q8_plan_create(q8_kind kind, q8_dtype g_dtype, const q8_tensor* t8, int32_t n8, const q8_tensor32* t32,
+                         int32_t n32, int32_t blocksize, q8_plan** out);
+
+/* Re-point the gradients: g_host[k] (a HOST array of n8 + n32 device pointers, 16-B aligned,
+ * g_dtype) becomes tensor k's gradient; a NULL entry keeps the previous pointer.  Host-only (no
+ * CUDA call), so it may run while earlier steps are in flight; takes effect at the next step call.
+ * Errors: INVALID for count != n8 + n32 or a misaligned pointer. */
+q8_status q8_plan_set_grads(q8_plan* plan, const void* const* g_host, int32_t count);
+
+/* One step of every tensor of the plan with the host step counter `step` (>= 1, as
+ * q8_optim8bit_step): one kernel launch per 384 tensors on `stream`.  Must be called with the
+ * plan's device current (INVALID otherwise); hyper-parameters validated as q8_optim8bit_step. */
+q8_status q8_plan_step(q8_plan* plan, const q8_hparams* hp, int64_t step, void* stream);
+
+/* The same step with the step counter on the DEVICE (CUDA-graph capturable: no host value changes
+ * between replays): the launch reads t - 1 from *step_dev (int64, device memory, 0 before the first
+ * step), computes the scalars of G8-G10 for t on the device (in binary64, the same expressions as
+ * the host path; see DESIGN.md 6.8 for the pow() caveat) and stores t back into *step_dev when it
+ * completes.  Hyper-parameters are captured by value at the call. */
+q8_status q8_plan_step_device(q8_plan* plan, const q8_hparams* hp, int64_t* step_dev, void* stream);
+
+/* Free the plan (host descriptors and its device counter).  NULL is a no-op. */
+void q8_plan_destroy(q8_plan* plan);
+
+/* Diagnostics: the fp32 scalars one update at `step` uses (G8-G10, LAMB L1), computed on the
+ * host -- out_host[10] = lr, beta1, beta2, 1-beta1, 1-beta2, step_size, eps_hat, wd, decay,
+ * fast-path flag (as a float) -- and the same ten for each steps_dev[i] computed on the DEVICE
+ * (out_dev[10 * n], device memory) by the code the capturable plan step runs. */
+q8_status q8_step_scalars(q8_kind kind, const q8_hparams* hp, int64_t step, float* out_host);
+q8_status q8_step_scalars_device(q8_kind kind, const q8_hparams* hp, const int64_t* steps_dev, int64_t n,
+                                 float* out_dev, void* stream);
 
 /* Thread-local description of the last error ("" after success). */
 const char* q8_last_error(void);

@@ -63,9 +63,9 @@ def lib():
         l.oracle_optim8bit_step.argtypes = [ctypes.c_int, f32p, f32p, u8p, u8p, f32p, f32p, i64, i64,
                                             ctypes.POINTER(_HParams), i64, ctypes.c_int]
         l.oracle_optim32bit_layerwise_step.argtypes = [ctypes.c_int, f32p, f32p, f32p, f32p, i64,
-                                                       ctypes.POINTER(_HParams), ctypes.c_double, i64, f32p]
+                                                       ctypes.POINTER(_HParams), ctypes.c_double, i64, f32p, f32p]
         l.oracle_optim8bit_layerwise_step.argtypes = [ctypes.c_int, f32p, f32p, u8p, u8p, f32p, f32p, i64, i64,
-                                                      ctypes.POINTER(_HParams), ctypes.c_double, i64, f32p]
+                                                      ctypes.POINTER(_HParams), ctypes.c_double, i64, f32p, f32p]
         _lib = l
     return _lib
 
@@ -77,6 +77,11 @@ def _f32(a) -> np.ndarray:
 
 def _ptr(a: np.ndarray, ct):
     return a.ctypes.data_as(ctypes.POINTER(ct))
+
+
+def _opt_ptr(a):
+    """float32 pointer or NULL (the returned pointer keeps the array alive)."""
+    return None if a is None else _ptr(a, ctypes.c_float)
 
 
 def dynamic_codebook(signed: bool) -> np.ndarray:
@@ -171,10 +176,15 @@ def optim8bit_step(kind, p, g, s1, s2, absmax1, absmax2, *, lr, beta1=0.9, beta2
         raise ValueError("invalid arguments")
 
 
+def _forced(scale):
+    return None if scale is None else np.array([scale], np.float32)
+
+
 def optim32bit_layerwise_step(kind, p, g, m, r, *, lr, beta1=0.9, beta2=0.999, eps=1e-6, weight_decay=0.0,
-                              bias_correction=True, step=1, trust_coefficient=0.001):
+                              bias_correction=True, step=1, trust_coefficient=0.001, forced_scale=None):
     """In-place 32-bit LAMB / LARS step over ONE tensor (readings L1-L4 in oracle.c).  p, m, r
-    float32 (r LAMB only).  Returns the fp32 per-tensor scale RN(lr*trust ratio)."""
+    float32 (r LAMB only).  Returns the fp32 per-tensor scale RN(lr*trust ratio).  forced_scale:
+    use this fp32 scale instead of the one from the norms (teacher forcing, reading L3)."""
     kind = KINDS.get(kind, kind)
     for a in (p, m) + ((r,) if kind == LAMB else ()):
         assert a.dtype == np.float32 and a.flags.c_contiguous
@@ -186,7 +196,7 @@ def optim32bit_layerwise_step(kind, p, g, m, r, *, lr, beta1=0.9, beta2=0.999, e
     rc = lib().oracle_optim32bit_layerwise_step(kind, _ptr(p, ctypes.c_float), _ptr(g, ctypes.c_float),
                                                 _ptr(m, ctypes.c_float), _ptr(r, ctypes.c_float), p.size,
                                                 ctypes.byref(hp), float(trust_coefficient), int(step),
-                                                _ptr(out, ctypes.c_float))
+                                                _ptr(out, ctypes.c_float), _opt_ptr(_forced(forced_scale)))
     if rc != 0:
         raise ValueError("invalid arguments")
     return out[0]
@@ -194,9 +204,9 @@ def optim32bit_layerwise_step(kind, p, g, m, r, *, lr, beta1=0.9, beta2=0.999, e
 
 def optim8bit_layerwise_step(kind, p, g, s1, s2, absmax1, absmax2, *, lr, beta1=0.9, beta2=0.999, eps=1e-6,
                              weight_decay=0.0, bias_correction=True, step=1, trust_coefficient=0.001,
-                             blocksize=2048):
+                             blocksize=2048, forced_scale=None):
     """In-place 8-bit LAMB / LARS step over ONE tensor (s2/absmax2 LAMB only).  Returns the
-    fp32 per-tensor scale."""
+    fp32 per-tensor scale.  forced_scale: as optim32bit_layerwise_step."""
     kind = KINDS.get(kind, kind)
     for a, dt in ((p, np.float32), (s1, np.uint8), (absmax1, np.float32)):
         assert a.dtype == dt and a.flags.c_contiguous
@@ -210,7 +220,7 @@ def optim8bit_layerwise_step(kind, p, g, s1, s2, absmax1, absmax2, *, lr, beta1=
                                                _ptr(s1, ctypes.c_uint8), _ptr(s2, ctypes.c_uint8),
                                                _ptr(absmax1, ctypes.c_float), _ptr(absmax2, ctypes.c_float),
                                                p.size, blocksize, ctypes.byref(hp), float(trust_coefficient),
-                                               int(step), _ptr(out, ctypes.c_float))
+                                               int(step), _ptr(out, ctypes.c_float), _opt_ptr(_forced(forced_scale)))
     if rc != 0:
         raise ValueError("invalid arguments")
     return out[0]

@@ -386,9 +386,13 @@ static double sum_squares(const float* x, int64_t n) {
 }
 
 /* 32-bit layer-wise step over ONE tensor (the layer).  m, r fp32 states (r LAMB only);
- * *scale_out (may be NULL) receives the fp32 per-tensor scale RN(lr*ratio) / RN(lr*local). */
+ * *scale_out (may be NULL) receives the fp32 per-tensor scale RN(lr*ratio) / RN(lr*local).
+ * scale_in (may be NULL) teacher-forces that scale instead of computing it from the norms: the
+ * norms are binary64 sums whose order reading L3 leaves open, so two correct implementations may
+ * round the scale differently in its last bit; given the same scale every other output is unique. */
 int oracle_optim32bit_layerwise_step(int kind, float* p, const float* g, float* m, float* r, int64_t n,
-                                     const oracle_hparams* hp, double trust_coeff, int64_t step, float* scale_out) {
+                                     const oracle_hparams* hp, double trust_coeff, int64_t step, float* scale_out,
+                                     const float* scale_in) {
     if ((kind != ORACLE_LAMB && kind != ORACLE_LARS) || n < 0 || step < 1) return -1;
     const float beta1 = (float)hp->beta1, wd = (float)hp->weight_decay;
     float a;
@@ -411,13 +415,13 @@ int oracle_optim32bit_layerwise_step(int kind, float* p, const float* g, float* 
         }
         double wn = sqrt(sum_squares(p, n)), un = sqrt(sum_squares(u, n));
         double ratio = (wn > 0.0 && un > 0.0) ? wn / un : 1.0; /* trust ratio */
-        a = (float)(hp->lr * ratio);
+        a = scale_in ? *scale_in : (float)(hp->lr * ratio);
         for (int64_t i = 0; i < n; i++) p[i] = p[i] - a * u[i];
         free(u);
     } else {
         double wn = sqrt(sum_squares(p, n)), gn = sqrt(sum_squares(g, n));
         double local = (wn > 0.0 && gn > 0.0) ? trust_coeff * wn / (gn + hp->weight_decay * wn) : 1.0;
-        a = (float)(hp->lr * local);
+        a = scale_in ? *scale_in : (float)(hp->lr * local);
         for (int64_t i = 0; i < n; i++) {
             float t = g[i] + wd * p[i];
             t = a * t;
@@ -434,7 +438,7 @@ int oracle_optim32bit_layerwise_step(int kind, float* p, const float* g, float* 
  * (LAMB only, G14). */
 int oracle_optim8bit_layerwise_step(int kind, float* p, const float* g, uint8_t* s1, uint8_t* s2, float* absmax1,
                                     float* absmax2, int64_t n, int64_t B, const oracle_hparams* hp, double trust_coeff,
-                                    int64_t step, float* scale_out) {
+                                    int64_t step, float* scale_out, const float* scale_in) {
     if ((kind != ORACLE_LAMB && kind != ORACLE_LARS) || n < 0 || B < 1 || step < 1) return -1;
     float Qs[256], Qu[256];
     if (oracle_dynamic_codebook(1, Qs) != 0 || oracle_dynamic_codebook(0, Qu) != 0) return -1;
@@ -443,7 +447,7 @@ int oracle_optim8bit_layerwise_step(int kind, float* p, const float* g, uint8_t*
     float* r = (float*)malloc(bytes);
     oracle_dequantize_blockwise(Qs, s1, absmax1, n, B, m);
     if (kind == ORACLE_LAMB) oracle_dequantize_blockwise(Qu, s2, absmax2, n, B, r);
-    int rc = oracle_optim32bit_layerwise_step(kind, p, g, m, r, n, hp, trust_coeff, step, scale_out);
+    int rc = oracle_optim32bit_layerwise_step(kind, p, g, m, r, n, hp, trust_coeff, step, scale_out, scale_in);
     if (rc == 0) {
         oracle_quantize_blockwise(Qs, m, n, B, absmax1, s1);
         if (kind == ORACLE_LAMB) oracle_quantize_blockwise(Qu, r, n, B, absmax2, s2);

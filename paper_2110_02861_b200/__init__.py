@@ -18,11 +18,12 @@ __all__ = [
 ]
 from ._binding import layerwise_workspace_bytes, optim8bit_step_layerwise, optim32bit_step_multi  # noqa: E402
 from ._binding import count_nonfinite, create_quantile_codebook, estimate_quantiles, quantiles_workspace_bytes  # noqa: E402
+from ._binding import Plan, step_scalars, step_scalars_device  # noqa: E402
 from .modules import StableEmbedding  # noqa: E402
 from .optim import LAMB8bit, LARS8bit, Adam8bit, AdamW8bit, Momentum8bit, state_bytes  # noqa: E402
 from .zero import Zero1Optimizer8bit, ZeroFusedOptimizer8bit, padded_numel, shard_range  # noqa: E402
 
-__all__ += ["count_nonfinite", "create_quantile_codebook", "estimate_quantiles", "quantiles_workspace_bytes",
+__all__ += ["Plan", "step_scalars", "step_scalars_device", "count_nonfinite", "create_quantile_codebook", "estimate_quantiles", "quantiles_workspace_bytes",
             "layerwise_workspace_bytes", "optim8bit_step_layerwise", "LAMB8bit", "LARS8bit",
             "optim32bit_step_multi", "StableEmbedding", "Adam8bit", "AdamW8bit", "Momentum8bit", "state_bytes", "Zero1Optimizer8bit", "ZeroFusedOptimizer8bit", "padded_numel",
             "shard_range"]

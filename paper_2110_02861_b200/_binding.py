@@ -27,7 +27,9 @@ EXPORTS = ("q8_create_dynamic_codebook", "q8_create_linear_codebook", "q8_quanti
            "q8_optim8bit_step", "q8_optim8bit_step_multi", "q8_optim32bit_step_multi",
            "q8_optim8bit_step_layerwise", "q8_layerwise_workspace_bytes", "q8_optim8bit_step_zero_fused",
            "q8_zero_signal_bytes", "q8_estimate_quantiles", "q8_quantiles_workspace_bytes",
-           "q8_create_quantile_codebook", "q8_count_nonfinite", "q8_last_error", "q8_version")
+           "q8_create_quantile_codebook", "q8_count_nonfinite", "q8_plan_create", "q8_plan_set_grads",
+           "q8_plan_step", "q8_plan_step_device", "q8_step_scalars", "q8_step_scalars_device",
+           "q8_plan_destroy", "q8_last_error", "q8_version")
 
 
 class Q8Error(RuntimeError):
@@ -79,8 +81,17 @@ def _load():
     lib.q8_quantiles_workspace_bytes.argtypes = [i64]
     lib.q8_create_quantile_codebook.argtypes = [vp, vp]
     lib.q8_count_nonfinite.argtypes = [vp, i32, i64, vp, vp]
-    for f in EXPORTS[:-2]:
+    lib.q8_plan_create.argtypes = [i32, i32, ctypes.POINTER(TensorDesc), i32, ctypes.POINTER(TensorDesc32), i32, i32,
+                                   ctypes.POINTER(vp)]
+    lib.q8_plan_set_grads.argtypes = [vp, ctypes.POINTER(vp), i32]
+    lib.q8_plan_step.argtypes = [vp, ctypes.POINTER(HParams), i64, vp]
+    lib.q8_plan_step_device.argtypes = [vp, ctypes.POINTER(HParams), vp, vp]
+    lib.q8_plan_destroy.argtypes = [vp]
+    lib.q8_step_scalars.argtypes = [i32, ctypes.POINTER(HParams), i64, vp]
+    lib.q8_step_scalars_device.argtypes = [i32, ctypes.POINTER(HParams), vp, i64, vp, vp]
+    for f in EXPORTS[:-3]:
         getattr(lib, f).restype = ctypes.c_int
+    lib.q8_plan_destroy.restype = None
     lib.q8_layerwise_workspace_bytes.restype = i64
     lib.q8_zero_signal_bytes.restype = i64
     lib.q8_quantiles_workspace_bytes.restype = i64
@@ -464,3 +475,98 @@ def count_nonfinite(g: torch.Tensor, out: torch.Tensor | None = None) -> torch.T
         _check(lib.q8_count_nonfinite(_dev_ptr(g, None, "g"), GDTYPES[g.dtype], g.numel(),
                                       _dev_ptr(out, torch.int64, "out", dev), _stream(dev)))
     return out
+
+
+def step_scalars(kind, hp: HParams, step: int) -> torch.Tensor:
+    """Host diagnostics: the ten fp32 scalars of one update (q8_step_scalars)."""
+    out = torch.empty(10, dtype=torch.float32)
+    _check(lib.q8_step_scalars(KINDS.get(kind, kind), ctypes.byref(hp), int(step), out.data_ptr()))
+    return out
+
+
+def step_scalars_device(kind, hp: HParams, steps: torch.Tensor) -> torch.Tensor:
+    """The same ten scalars for every int64 step of `steps` (CUDA), computed on the device by the code
+    the capturable plan step runs (q8_step_scalars_device); returns [n, 10] float32 on the device."""
+    dev = steps.device
+    out = torch.empty(steps.numel(), 10, dtype=torch.float32, device=dev)
+    with _on(dev):
+        _check(lib.q8_step_scalars_device(KINDS.get(kind, kind), ctypes.byref(hp), _dev_ptr(steps, torch.int64, "steps"),
+                                          steps.numel(), _dev_ptr(out, torch.float32, "out", dev), _stream(dev)))
+    return out
+
+
+class Plan:
+    """A prepared multi-tensor step (q8_plan_*): the descriptors of every tensor are validated and
+    kept by the library once; a step is one call (one launch per 384 tensors).  entries8: (p, g, s1,
+    s2_or_None, absmax1, absmax2_or_None); entries32: (p, g, m, r_or_None) -- tensors whose states
+    stay fp32 (the Stable Embedding, S3.3 P:124), stepped in the SAME launch.  Tensor k of the plan is
+    entries8[k], then entries32."""
+
+    def __init__(self, kind, entries8=(), entries32=()):
+        self.kind = KINDS.get(kind, kind)
+        entries8, entries32 = list(entries8), list(entries32)
+        alle = entries8 + entries32
+        if not alle:
+            raise ValueError("a plan needs at least one tensor")
+        self.device = alle[0][0].device
+        self.count = len(alle)
+        tl = TensorList(entries8, self.kind) if entries8 else None
+        gd = tl.gdtype if tl else None
+        arr32 = (TensorDesc32 * max(1, len(entries32)))()
+        dev = self.device
+        for i, (p, g, m, r) in enumerate(entries32):
+            n = p.numel()
+            if g.numel() != n or m.numel() != n or (r is not None and r.numel() != n) or \
+                    (self.kind != Q8_MOMENTUM and r is None):
+                raise ValueError(f"32-bit tensor {i}: size mismatch")
+            if GDTYPES.get(g.dtype) is None or (gd is not None and GDTYPES[g.dtype] != gd):
+                raise ValueError("all gradients of one plan must share a dtype")
+            gd = GDTYPES[g.dtype]
+            arr32[i] = TensorDesc32(_dev_ptr(p, torch.float32, "p", dev), _dev_ptr(g, None, "g", dev),
+                                    _dev_ptr(m, torch.float32, "m", dev), _dev_ptr(r, torch.float32, "r", dev), n)
+        self.gdtype = gd
+        self._gdt_torch = {v: k for k, v in GDTYPES.items()}[gd]
+        self._numel = [e[0].numel() for e in alle]
+        self.keep = alle  # the library holds raw pointers: keep every tensor alive
+        h = ctypes.c_void_p()
+        with _on(dev):
+            _check(lib.q8_plan_create(self.kind, gd, tl.arr if tl else None, len(entries8), arr32, len(entries32),
+                                      BLOCKSIZE, ctypes.byref(h)))
+        self._h = h
+        self._gptr = (ctypes.c_void_p * self.count)()
+
+    def set_grads(self, grads):
+        """Re-point the gradients (same count, sizes, dtype and device as the plan's)."""
+        if len(grads) != self.count:
+            raise ValueError("gradient count changed")
+        gdt, dev = self._gdt_torch, self.device
+        for i, (g, n) in enumerate(zip(grads, self._numel)):
+            if g.dtype != gdt or g.device != dev or g.numel() != n or not g.is_contiguous():
+                raise ValueError(f"tensor {i}: gradient dtype/device/size changed or not contiguous")
+        self.set_grad_ptrs([g.data_ptr() for g in grads], grads)
+
+    def set_grad_ptrs(self, ptrs, keep=None):
+        """Re-point the gradients by address (the caller has checked dtype, size, device and
+        contiguity -- the optimizer's fast path); `keep` is held until the next refresh."""
+        self._gptr[:] = ptrs
+        _check(lib.q8_plan_set_grads(self._h, self._gptr, self.count))
+        self.grads = keep
+
+    def step(self, hp: HParams, step: int):
+        with _on(self.device):
+            _check(lib.q8_plan_step(self._h, ctypes.byref(hp), int(step), _stream(self.device)))
+
+    def step_device(self, hp: HParams, step_t: torch.Tensor):
+        """Capturable step: t - 1 is read from step_t (int64 CUDA tensor of one element) on the device
+        and t is stored back when the step completes; no host value changes between calls, so the
+        call can be captured in a CUDA graph."""
+        with _on(self.device):
+            _check(lib.q8_plan_step_device(self._h, ctypes.byref(hp), _dev_ptr(step_t, torch.int64, "step",
+                                                                                 self.device),
+                                           _stream(self.device)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and lib is not None:
+            lib.q8_plan_destroy(h)
+            self._h = None

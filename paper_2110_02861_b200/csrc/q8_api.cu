@@ -7,8 +7,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/q8.h"
 #include "q8_kernels.cuh"
@@ -140,34 +142,7 @@ q8_status reject_layerwise(q8_kind kind) {
 
 // fp32 scalars of the update, computed in double and rounded once (G8-G10; LAMB L1).
 q8::StepScalars make_scalars(const q8_hparams* hp, int64_t step, q8_kind kind = Q8_ADAM) {
-    q8::StepScalars s;
-    s.lr = static_cast<float>(hp->lr);
-    s.beta1 = static_cast<float>(hp->beta1);
-    s.beta2 = static_cast<float>(hp->beta2);
-    s.omb1 = static_cast<float>(1.0 - hp->beta1);
-    s.omb2 = static_cast<float>(1.0 - hp->beta2);
-    if (hp->bias_correction) {
-        // Kingma & Ba's folded bias correction: alpha_t = alpha sqrt(1 - b2^t) / (1 - b1^t),
-        // eps_hat = eps sqrt(1 - b2^t)  (G8)
-        const double bc1 = 1.0 - std::pow(hp->beta1, static_cast<double>(step));
-        const double bc2 = 1.0 - std::pow(hp->beta2, static_cast<double>(step));
-        s.step_size = static_cast<float>(hp->lr * std::sqrt(bc2) / bc1);
-        s.eps_hat = static_cast<float>(hp->eps * std::sqrt(bc2));
-    } else {
-        s.step_size = static_cast<float>(hp->lr);
-        s.eps_hat = static_cast<float>(hp->eps);
-    }
-    s.wd = static_cast<float>(hp->weight_decay);
-    s.decay = static_cast<float>(1.0 - hp->lr * hp->weight_decay);
-    if (kind == Q8_LAMB) {
-        // LAMB: u = c*d + wd*w with the bias-correction factor c alone; lr enters the trust scale
-        s.step_size = hp->bias_correction ? static_cast<float>(
-                                                std::sqrt(1.0 - std::pow(hp->beta2, static_cast<double>(step))) /
-                                                (1.0 - std::pow(hp->beta1, static_cast<double>(step))))
-                                          : 1.0f;
-    }
-    s.fast_div = (s.eps_hat >= 0x1p-40f && std::isfinite(s.eps_hat)) ? 1 : 0;
-    return s;
+    return q8::compute_scalars(kind, hp->lr, hp->beta1, hp->beta2, hp->eps, hp->weight_decay, hp->bias_correction, step);
 }
 
 q8_status validate_tensor(q8_kind kind, q8_dtype gdt, const q8_tensor& t, int idx) {
@@ -219,13 +194,13 @@ int g_smem_count = 0;
 
 template <int MAXT>
 q8_status dispatch_step(q8_kind kind, q8_dtype gdt, const q8::StepParams<MAXT>& P, const DeviceState* d,
-                        cudaStream_t st) {
+                        cudaStream_t st, int plan = 0) {
     static const int subt = [] {
         const char* e = std::getenv("Q8_SUBT");
         const int v = e ? std::atoi(e) : 0;
         return (v == 128 || v == 256) ? v : 0;
     }();
-    const q8::LaunchCtx ctx{d->tabs, d->sms, st, search_variant(), nsub_variant(gdt), subt};
+    const q8::LaunchCtx ctx{d->tabs, d->sms, st, search_variant(), nsub_variant(gdt), subt, plan};
     const q8::StepParams<1>* single = nullptr;
     const q8::StepParams<q8::kMultiMaxT>* multi = nullptr;
     if constexpr (MAXT == 1) single = &P; else multi = &P;
@@ -792,6 +767,201 @@ q8_status q8_optim8bit_step_zero_fused(q8_kind kind, q8_dtype g_dtype, int32_t w
         case Q8_BF16: e = q8::launch_zero_g2(kind, P, ctx, grid); break;
     }
     if (e != cudaSuccess) return cuda_fail(e, "fused ZeRO step launch");
+    return ok();
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- plans (prepared multi-tensor steps)
+
+struct q8_plan {
+    int dev = 0;
+    q8_kind kind = Q8_ADAM;
+    q8_dtype gdt = Q8_F32;
+    int32_t count = 0;
+    std::vector<std::unique_ptr<q8::StepParams<q8::kMultiMaxT>>> chunks;
+    std::vector<int32_t> chunk_of, slot_of;  // per plan tensor; -1 for empty tensors
+    unsigned int* done = nullptr;             // CTA completion counter of capturable launches
+};
+
+namespace {
+
+__global__ void step_scalars_kernel(int kind, double lr, double beta1, double beta2, double eps, double wd, int bc,
+                                    const int64_t* steps, int64_t n, float* out) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const q8::StepScalars s = q8::compute_scalars(kind, lr, beta1, beta2, eps, wd, bc, steps[i]);
+        float* o = out + 10 * i;
+        o[0] = s.lr; o[1] = s.beta1; o[2] = s.beta2; o[3] = s.omb1; o[4] = s.omb2;
+        o[5] = s.step_size; o[6] = s.eps_hat; o[7] = s.wd; o[8] = s.decay; o[9] = static_cast<float>(s.fast_div);
+    }
+}
+
+q8_status plan_device_check(const q8_plan* plan) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev != plan->dev)
+        return fail(Q8_ERR_INVALID, "plan was built on device %d but device %d is current", plan->dev, dev);
+    return Q8_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+q8_status q8_plan_create(q8_kind kind, q8_dtype g_dtype, const q8_tensor* t8, int32_t n8, const q8_tensor32* t32,
+                         int32_t n32, int32_t blocksize, q8_plan** out) {
+    if (!out) return fail(Q8_ERR_INVALID, "out is NULL");
+    *out = nullptr;
+    if (q8_status s = reject_layerwise(kind); s != Q8_OK) return s;
+    if (kind != Q8_ADAM && kind != Q8_ADAMW && kind != Q8_MOMENTUM) return fail(Q8_ERR_INVALID, "bad kind %d", kind);
+    if (q8_status s = check_common(g_dtype, blocksize); s != Q8_OK) return s;
+    if (n8 < 0 || n32 < 0) return fail(Q8_ERR_INVALID, "tensor counts must be >= 0");
+    if ((n8 > 0 && !t8) || (n32 > 0 && !t32)) return fail(Q8_ERR_INVALID, "tensor array is NULL");
+    for (int i = 0; i < n8; ++i)
+        if (q8_status s = validate_tensor(kind, g_dtype, t8[i], i); s != Q8_OK) return s;
+    for (int i = 0; i < n32; ++i)
+        if (q8_status s = validate_tensor32(kind, t32[i], n8 + i); s != Q8_OK) return s;
+    DeviceState* d = nullptr;
+    if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    auto plan = std::make_unique<q8_plan>();
+    cudaError_t e = cudaGetDevice(&plan->dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    plan->kind = kind;
+    plan->gdt = g_dtype;
+    plan->count = n8 + n32;
+    plan->chunk_of.assign(plan->count, -1);
+    plan->slot_of.assign(plan->count, -1);
+    constexpr int MAXT = q8::kMultiMaxT;
+    q8::StepParams<MAXT>* P = nullptr;
+    int64_t blocks = 0;
+    for (int k = 0; k < plan->count; ++k) {
+        q8::TensorDesc T;
+        if (k < n8) {
+            const q8_tensor& t = t8[k];
+            T = q8::TensorDesc{t.p, t.g, t.s1, t.s2, t.absmax1, t.absmax2, t.n};
+        } else {  // 32-bit states: a1 == NULL marks the tensor, s1/s2 carry m/r (TensorDesc)
+            const q8_tensor32& t = t32[k - n8];
+            T = q8::TensorDesc{t.p, t.g, reinterpret_cast<uint8_t*>(t.m), reinterpret_cast<uint8_t*>(t.r), nullptr,
+                               nullptr, t.n};
+        }
+        if (T.n == 0) continue;
+        if (!P || P->num_tensors == MAXT) {
+            plan->chunks.push_back(std::make_unique<q8::StepParams<MAXT>>());
+            P = plan->chunks.back().get();
+            P->scale = nullptr;
+            P->partial = nullptr;
+            P->num_tensors = 0;
+            blocks = 0;
+        }
+        const int slot = P->num_tensors++;
+        P->t[slot] = T;
+        P->block_start[slot] = blocks;
+        blocks += (T.n + q8::kBlock - 1) / q8::kBlock;
+        P->block_start[slot + 1] = blocks;
+        P->total_blocks = blocks;
+        plan->chunk_of[k] = static_cast<int32_t>(plan->chunks.size() - 1);
+        plan->slot_of[k] = slot;
+    }
+    e = cudaMalloc(&plan->done, sizeof(unsigned int));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(plan counter)");
+    e = cudaMemset(plan->done, 0, sizeof(unsigned int));
+    if (e != cudaSuccess) {
+        cudaFree(plan->done);
+        return cuda_fail(e, "cudaMemset(plan counter)");
+    }
+    *out = plan.release();
+    return ok();
+}
+
+q8_status q8_plan_set_grads(q8_plan* plan, const void* const* g_host, int32_t count) {
+    if (!plan || !g_host) return fail(Q8_ERR_INVALID, "NULL argument");
+    if (count != plan->count) return fail(Q8_ERR_INVALID, "count %d != the plan's %d tensors", count, plan->count);
+    for (int k = 0; k < count; ++k) {
+        const void* g = g_host[k];
+        if (!g || plan->chunk_of[k] < 0) continue;
+        if (!aligned(g, 16)) return fail(Q8_ERR_INVALID, "tensor %d: g not 16-byte aligned", k);
+        plan->chunks[plan->chunk_of[k]]->t[plan->slot_of[k]].g = g;
+    }
+    return ok();
+}
+
+q8_status q8_plan_step(q8_plan* plan, const q8_hparams* hp, int64_t step, void* stream) {
+    if (!plan) return fail(Q8_ERR_INVALID, "plan is NULL");
+    if (q8_status s = validate_hparams(plan->kind, hp, step); s != Q8_OK) return s;
+    if (q8_status s = plan_device_check(plan); s != Q8_OK) return s;
+    DeviceState* d = nullptr;
+    if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    const q8::StepScalars sc = make_scalars(hp, step);
+    for (auto& P : plan->chunks) {
+        P->s = sc;
+        P->ds.step = nullptr;
+        if (q8_status s =
+                dispatch_step<q8::kMultiMaxT>(plan->kind, plan->gdt, *P, d, static_cast<cudaStream_t>(stream), 1);
+            s != Q8_OK)
+            return s;
+    }
+    return ok();
+}
+
+q8_status q8_plan_step_device(q8_plan* plan, const q8_hparams* hp, int64_t* step_dev, void* stream) {
+    if (!plan || !step_dev) return fail(Q8_ERR_INVALID, "NULL argument");
+    if (q8_status s = validate_hparams(plan->kind, hp, 1); s != Q8_OK) return s;
+    if (!aligned(step_dev, 8)) return fail(Q8_ERR_INVALID, "step_dev not 8-byte aligned");
+    if (q8_status s = plan_device_check(plan); s != Q8_OK) return s;
+    DeviceState* d = nullptr;
+    if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    const size_t nc = plan->chunks.size();
+    for (size_t c = 0; c < nc; ++c) {
+        auto& P = plan->chunks[c];
+        P->s = make_scalars(hp, 1);  // placeholder; the kernel uses ds (its wd decides the L2 variant)
+        P->ds.step = step_dev;
+        P->ds.done = plan->done;
+        P->ds.advance = c + 1 == nc ? 1 : 0;
+        P->ds.kind = plan->kind;
+        P->ds.lr = hp->lr;
+        P->ds.beta1 = hp->beta1;
+        P->ds.beta2 = hp->beta2;
+        P->ds.eps = hp->eps;
+        P->ds.wd = hp->weight_decay;
+        P->ds.bias_correction = hp->bias_correction;
+        q8_status s =
+            dispatch_step<q8::kMultiMaxT>(plan->kind, plan->gdt, *P, d, static_cast<cudaStream_t>(stream), 1);
+        P->ds.step = nullptr;
+        if (s != Q8_OK) return s;
+    }
+    return ok();
+}
+
+void q8_plan_destroy(q8_plan* plan) {
+    if (!plan) return;
+    if (plan->done) cudaFree(plan->done);
+    delete plan;
+}
+
+q8_status q8_step_scalars(q8_kind kind, const q8_hparams* hp, int64_t step, float* out_host) {
+    if (!out_host) return fail(Q8_ERR_INVALID, "out_host is NULL");
+    if (q8_status s = validate_hparams(kind, hp, step); s != Q8_OK) return s;
+    const q8::StepScalars s = make_scalars(hp, step, kind);
+    const float v[10] = {s.lr, s.beta1, s.beta2, s.omb1, s.omb2, s.step_size, s.eps_hat, s.wd, s.decay,
+                         static_cast<float>(s.fast_div)};
+    std::memcpy(out_host, v, sizeof v);
+    return ok();
+}
+
+q8_status q8_step_scalars_device(q8_kind kind, const q8_hparams* hp, const int64_t* steps_dev, int64_t n,
+                                 float* out_dev, void* stream) {
+    if (q8_status s = validate_hparams(kind, hp, 1); s != Q8_OK) return s;
+    if (n < 0) return fail(Q8_ERR_INVALID, "n < 0");
+    if (n == 0) return ok();
+    if (!steps_dev || !out_dev) return fail(Q8_ERR_INVALID, "NULL buffer with n > 0");
+    if (!aligned(steps_dev, 8) || !aligned(out_dev, 4)) return fail(Q8_ERR_INVALID, "misaligned buffer");
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 1024));
+    step_scalars_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        kind, hp->lr, hp->beta1, hp->beta2, hp->eps, hp->weight_decay, hp->bias_correction, steps_dev, n, out_dev);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "step_scalars_kernel launch");
     return ok();
 }
 

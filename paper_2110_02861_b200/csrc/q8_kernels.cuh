@@ -64,6 +64,9 @@ constexpr int kTabBytes = kTabLut * 4 + kLutSBytes + kLutUBytes;
 constexpr int kTabFloats = kTabBytes / 4;
 constexpr int SEARCH_EYTZINGER = 0, SEARCH_BUCKET = 1;
 
+// One tensor of a launch.  8-bit states: s1/s2 codes, a1/a2 absmax.  In multi-tensor launches a
+// tensor with a1 == NULL keeps 32-bit states (the Stable Embedding, S3.3 P:124): s1/s2 then hold
+// its fp32 m / r arrays.
 struct TensorDesc {
     float* p;
     const void* g;
@@ -74,10 +77,60 @@ struct TensorDesc {
     int64_t n;
 };
 
-struct StepScalars {       // all computed on the host in double, rounded once (G8-G10)
+struct StepScalars {       // all computed in double and rounded once (G8-G10)
     // step_size: alpha_t for Adam/AdamW; for LAMB the bias-correction factor c alone (L1)
     float lr, beta1, beta2, omb1, omb2, step_size, eps_hat, wd, decay;
     int fast_div;          // eps_hat >= 2^-40: the packed sqrt/div fast path may be used
+};
+
+// The fp32 scalars of one update at step t (1-based), from the double hyper-parameters: one
+// source for the host (every host-stepped launch) and the device (capturable launches that read t
+// from device memory, DeviceStep).  Readings G8 (Kingma & Ba's folded bias correction
+// alpha_t = alpha sqrt(1 - b2^t)/(1 - b1^t), eps_hat = eps sqrt(1 - b2^t)), G10 (decay = 1 - lr wd)
+// and, for LAMB, L1 (step_size = the bias-correction factor c alone).  Every expression is
+// evaluated in binary64 (no contraction: the library is built with -fmad=false) and rounded once.
+// Host and device differ only in the pow() implementation (glibc vs CUDA's libdevice, both within
+// 1-2 double ulps), which can change an fp32 result only if the double value lies within ~2^-51
+// relative of an fp32 rounding boundary; tests/test_gpu_plan.py compares both for t = 1 .. 2^20.
+__host__ __device__ inline StepScalars compute_scalars(int kind, double lr, double beta1, double beta2, double eps,
+                                                       double wd, int bias_correction, int64_t step) {
+    StepScalars s;
+    s.lr = static_cast<float>(lr);
+    s.beta1 = static_cast<float>(beta1);
+    s.beta2 = static_cast<float>(beta2);
+    s.omb1 = static_cast<float>(1.0 - beta1);
+    s.omb2 = static_cast<float>(1.0 - beta2);
+    if (bias_correction) {
+        const double bc1 = 1.0 - pow(beta1, static_cast<double>(step));
+        const double bc2 = 1.0 - pow(beta2, static_cast<double>(step));
+        s.step_size = static_cast<float>(lr * sqrt(bc2) / bc1);
+        s.eps_hat = static_cast<float>(eps * sqrt(bc2));
+    } else {
+        s.step_size = static_cast<float>(lr);
+        s.eps_hat = static_cast<float>(eps);
+    }
+    s.wd = static_cast<float>(wd);
+    s.decay = static_cast<float>(1.0 - lr * wd);
+    if (kind == 3 /* KIND_LAMB */) {
+        s.step_size = bias_correction ? static_cast<float>(sqrt(1.0 - pow(beta2, static_cast<double>(step))) /
+                                                           (1.0 - pow(beta1, static_cast<double>(step))))
+                                      : 1.0f;
+    }
+    s.fast_div = (s.eps_hat >= 0x1p-40f && isfinite(s.eps_hat)) ? 1 : 0;
+    return s;
+}
+
+// Capturable step (q8_plan_step_device): the launch reads t - 1 from *step (device int64) and
+// computes its scalars on the device; the last CTA to finish the launch that carries `advance`
+// stores t back (a CTA-completion counter, reset to 0 by that CTA), so a whole optimizer step can be
+// captured in a CUDA graph and replayed with no host work.
+struct DeviceStep {
+    int64_t* step = nullptr;  // NULL: host scalars (StepParams::s) are used
+    unsigned int* done;    // CTA completion counter, 0 between launches
+    int advance;           // this launch stores *step = t at its end
+    int kind;
+    double lr, beta1, beta2, eps, wd;
+    int bias_correction;
 };
 
 // Fused ZeRO-1 step over peer memory: every rank's full padded
@@ -100,6 +153,7 @@ struct ZeroParams {
 template <int MAXT>
 struct StepParams {
     StepScalars s;
+    DeviceStep ds;                  // multi-tensor plans only (ds.step NULL otherwise)
     const float* scale;             // LAMB / LARS: per-tensor trust scale RN(lr*ratio) (L1-L3)
     double2* partial;               // LAMB norms pass: per-block (sum w^2, sum u^2)
     ZeroParams z;                   // fused ZeRO-1 mode only

@@ -15,6 +15,7 @@ struct LaunchCtx {
     int search;  // SEARCH_BUCKET or SEARCH_EYTZINGER
     int nsub;    // 2, 3 or 4 sub-blocks per CTA
     int subt;    // threads per sub-block (128 or 256); 0 = default for the gradient dtype
+    int plan = 0;  // multi-tensor plan launch (mixed 32-bit states, shared-memory / device scalars)
 };
 
 constexpr int kMultiMaxT = 384;

@@ -48,6 +48,15 @@ cudaError_t launch_kind_t(const StepParams<MAXT>& P, const LaunchCtx& ctx) {
 
 template <int KIND, int MAXT>
 cudaError_t launch_kind(const StepParams<MAXT>& P, const LaunchCtx& ctx) {
+    if constexpr (MAXT > 1) {
+        if (ctx.plan) {  // plans: the default configuration only
+            constexpr int G = Q8_GDT;
+            constexpr int NS = G == G_F32 ? 3 : 4;
+            constexpr int SUBT = G == G_F32 ? 256 : 128;
+            return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, NS, SUBT, MODE_STEP, true>, NS, SUBT,
+                              P.total_blocks, ctx, P, ctx.tabs);
+        }
+    }
     const int subt = ctx.subt ? ctx.subt : (Q8_GDT == G_F32 ? 256 : 128);
     return subt == 128 ? launch_kind_t<KIND, MAXT, 128>(P, ctx) : launch_kind_t<KIND, MAXT, 256>(P, ctx);
 }
@@ -135,8 +144,20 @@ cudaError_t launch_zero_t(const StepParams<1>& P, const LaunchCtx& ctx, int grid
     const int smem = step_smem_bytes(NS, G);
     cudaError_t e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
     if (e != cudaSuccess) return e;
-    fn<<<static_cast<unsigned>(grid), NS * SUBT, smem, ctx.stream>>>(P, ctx.tabs);
-    return cudaGetLastError();
+    // Cooperative launch: the runtime guarantees (or refuses with
+    // cudaErrorCooperativeLaunchTooLarge) that every CTA of this grid is resident at once, so CTA i
+    // can never wait at the cross-rank flag barrier behind a CTA of its own rank that has no SM.
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(NS * SUBT);
+    cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+    cfg.stream = ctx.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, P, ctx.tabs);
 }
 }  // namespace
 

@@ -89,6 +89,9 @@ WORKLOADS = {
     # SURVEY 8(f) row 4 (App G): SRAM-Quantiles over a GPT-2-XL-sized fp32 buffer
     "quantiles_gpt2_xl": dict(kind="adamw", grad_dtype="float32", shapes=gpt2_shapes(1600, 48), quantiles=True,
                               desc="SRAM-Quantiles + Eq.5 codebook over a 1.5B fp32 GPT-2-XL-sized buffer"),
+    # the stand-alone block-wise codec over a GPT-2-XL-sized fp32 buffer
+    "codec_gpt2_xl": dict(kind="adam", grad_dtype="float32", shapes=gpt2_shapes(1600, 48), codec=True,
+                          desc="block-wise quantize (dynamic and generic table) + dequantize, 1.5B fp32 buffer"),
     "lars_resnet50": dict(kind="lars", grad_dtype="float16", shapes=resnet50_shapes(), layerwise=True,
                           desc="8-bit LARS, ResNet-50 161-tensor layer list, fp16 grads"),
 }

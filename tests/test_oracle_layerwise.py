@@ -176,3 +176,41 @@ def test_8bit_layerwise_tracks_32bit(kind):
     u8, u32 = p8.astype(np.float64) - p0, p32.astype(np.float64) - p0
     agg = np.sum(np.abs(u8 - u32)) / np.sum(np.abs(u32))
     assert agg <= 0.05, agg
+
+
+@pytest.mark.parametrize("kind", ["lamb", "lars"])
+def test_forced_scale_teacher_forcing(kind):
+    """Teacher forcing (reading L3): forcing the oracle's own scale reproduces the unforced step bit
+    for bit; a forced scale of 0 freezes LAMB's parameters (w - 0*u = w) while the moments still
+    advance exactly as in the unforced step, and reduces LARS to w - beta*v."""
+    n = 5000
+    hp = dict(synth.HPARAMS[kind])
+    eta = hp.pop("trust_coefficient", 0.001)
+    two = kind == "lamb"
+
+    def state():
+        p = synth.params(n, seed=3).numpy()
+        s1, a1 = (t.numpy() for t in synth.random_state(n, seed=4, scale=1e-3))
+        s2, a2 = (t.numpy() for t in synth.random_state(n, seed=5, scale=1e-6))
+        return [p, s1, s2 if two else None, a1, a2 if two else None]
+
+    g = synth.grads(n, step=2, seed=6).numpy()
+    a, b = state(), state()
+    sa = oracle.optim8bit_layerwise_step(kind, a[0], g, a[1], a[2], a[3], a[4], step=2, trust_coefficient=eta, **hp)
+    sb = oracle.optim8bit_layerwise_step(kind, b[0], g, b[1], b[2], b[3], b[4], step=2, trust_coefficient=eta,
+                                         forced_scale=sa, **hp)
+    assert sb == sa
+    for x, y in zip(a, b):
+        if x is not None:
+            assert np.array_equal(x.view(np.uint8), y.view(np.uint8))
+    c = state()
+    p0 = c[0].copy()
+    v0 = oracle.dequantize_blockwise(oracle.dynamic_codebook(True), c[1], c[3])
+    oracle.optim8bit_layerwise_step(kind, c[0], g, c[1], c[2], c[3], c[4], step=2, trust_coefficient=eta,
+                                    forced_scale=0.0, **hp)
+    if kind == "lamb":
+        assert np.array_equal(c[0], p0)
+        assert np.array_equal(c[1], a[1]) and np.array_equal(c[2], a[2])
+    else:
+        v = (np.float32(hp["beta1"]) * v0).astype(np.float32)
+        assert np.array_equal(c[0], (p0 - v).astype(np.float32))
