@@ -1164,7 +1164,7 @@ def main_codec(args, cfg, q8, world, rank, local, dev):
             "roofline": {"bound": "hbm", "achieved": k0["achieved_gbs"], "peak": peak, "unit": "GB/s",
                          "frac": k0["frac"], "traffic": traffic, "bytes_per_element": bpe,
                          "algorithmic_bytes_per_launch": n * bpe,
-                         "kernel": "quantize_blockwise_dynamic_kernel (the dominant launch of the step)",
+                         "kernel": "quantize_tma_kernel<BUILTIN, signed> (the dominant launch of the step)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
                          else "fallback 6.65 TB/s (B200_PROFILING.md)"},
             "kernels": kern, "dynamic_equals_generic": same,

@@ -247,6 +247,9 @@ int64_t q8_layerwise_workspace_bytes(const q8_tensor* tensors_host, int32_t num_
  *                     shard is read from p_peers_host[rank]
  *   sig_peers_host[r] rank r's signal pad, q8_zero_signal_bytes(world, num_ctas) bytes, zeroed once
  *                     at allocation and then owned by these calls
+ *   p_multicast       NULL, or the NVLS multicast address (NVSwitch, e.g. torch symmetric memory's
+ *                     multicast_ptr) that maps every rank's parameter buffer: the all-gather is then
+ *                     ONE multimem.st per 16 bytes instead of world peer stores (16-B aligned)
  *   s1, s2, absmax1, absmax2  this rank's shard states (n_pad/world codes, n_pad/world/2048 absmax)
  * (the three peer arrays are HOST arrays of device pointers, copied into the launch)
  * Reading Z1: g = (g_0 + ... + g_{world-1}) / world per element -- binary32 adds in rank order,
@@ -265,7 +268,8 @@ int64_t q8_layerwise_workspace_bytes(const q8_tensor* tensors_host, int32_t num_
  * world <= 16.  Errors: as q8_optim8bit_step, plus INVALID for bad world/rank/n_pad/epoch/num_ctas. */
 q8_status q8_optim8bit_step_zero_fused(q8_kind kind, q8_dtype g_dtype, int32_t world, int32_t rank,
                                        const void* const* g_peers_host, float* const* p_peers_host,
-                                       uint32_t* const* sig_peers_host, uint8_t* s1, uint8_t* s2, float* absmax1,
+                                       uint32_t* const* sig_peers_host, float* p_multicast, uint8_t* s1, uint8_t* s2,
+                                       float* absmax1,
                                        float* absmax2, int64_t n_pad, int32_t blocksize, const q8_hparams* hp,
                                        int64_t step, uint32_t epoch, int32_t num_ctas, void* stream);
 

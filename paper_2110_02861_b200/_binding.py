@@ -74,8 +74,8 @@ def _load():
                                                 ctypes.POINTER(HParams), ctypes.c_double, i64, vp, i64, vp]
     lib.q8_layerwise_workspace_bytes.argtypes = [ctypes.POINTER(TensorDesc), i32]
     lib.q8_optim8bit_step_zero_fused.argtypes = [i32, i32, i32, i32, ctypes.POINTER(vp), ctypes.POINTER(vp),
-                                                 ctypes.POINTER(vp), vp, vp, vp, vp, i64, i32, ctypes.POINTER(HParams),
-                                                 i64, ctypes.c_uint32, i32, vp]
+                                                 ctypes.POINTER(vp), vp, vp, vp, vp, vp, i64, i32,
+                                                 ctypes.POINTER(HParams), i64, ctypes.c_uint32, i32, vp]
     lib.q8_zero_signal_bytes.argtypes = [i32, i32]
     lib.q8_estimate_quantiles.argtypes = [vp, i64, vp, vp, vp, i64, vp]
     lib.q8_quantiles_workspace_bytes.argtypes = [i64]
@@ -405,15 +405,16 @@ def zero_signal_bytes(world: int, num_ctas: int = 0) -> int:
 
 
 def optim8bit_step_zero_fused(kind, world, rank, g_ptrs, p_ptrs, sig_ptrs, s1, s2, absmax1, absmax2, n_pad, g_dtype,
-                              *, step, epoch, num_ctas=0, stream=None, hp: HParams):
+                              *, step, epoch, num_ctas=0, stream=None, hp: HParams, p_multicast=None):
     """Fused ZeRO-1 step over peer memory (q8_optim8bit_step_zero_fused): g_ptrs / p_ptrs /
-    sig_ptrs are per-rank device addresses (ints) of the gradient, parameter and signal buffers."""
+    sig_ptrs are per-rank device addresses (ints) of the gradient, parameter and signal buffers;
+    p_multicast (int or None) the NVLS multicast address of the parameter buffers."""
     kind = KINDS.get(kind, kind)
     dev = s1.device
     arr = ctypes.c_void_p * world
     with _on(dev):
         _check(lib.q8_optim8bit_step_zero_fused(kind, GDTYPES[g_dtype], world, rank, arr(*g_ptrs), arr(*p_ptrs),
-                                                arr(*sig_ptrs), _dev_ptr(s1, torch.uint8, "s1"),
+                                                arr(*sig_ptrs), p_multicast, _dev_ptr(s1, torch.uint8, "s1"),
                                                 _dev_ptr(s2, torch.uint8, "s2", dev),
                                                 _dev_ptr(absmax1, torch.float32, "absmax1", dev),
                                                 _dev_ptr(absmax2, torch.float32, "absmax2", dev), int(n_pad),

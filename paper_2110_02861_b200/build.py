@@ -15,7 +15,7 @@ LIB = os.path.join(HERE, "libq8.so")
 OBJDIR = os.environ.get("Q8_OBJDIR", "/tmp/q8_build")
 UNITS = [("q8_api.cu", []), ("codebook_host.cpp", []),
          ("step_inst.cu", ["-DQ8_GDT=0"]), ("step_inst.cu", ["-DQ8_GDT=1"]), ("step_inst.cu", ["-DQ8_GDT=2"])]
-HEADERS = ["q8_kernels.cuh", "q8_codec.cuh", "q8_step32_kernel.cuh", "q8_step_kernel.cuh", "q8_layerwise.cuh", "q8_quantiles.cuh", "q8_launch.h", os.path.join("..", "..", "include", "q8.h")]
+HEADERS = ["q8_kernels.cuh", "q8_codec.cuh", "q8_step32_kernel.cuh", "q8_step_kernel.cuh", "q8_layerwise.cuh", "q8_quantiles.cuh", "q8_quant_kernel.cuh", "q8_launch.h", os.path.join("..", "..", "include", "q8.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [

@@ -19,6 +19,7 @@
 #include "q8_step_kernel.cuh"
 #include "q8_step32_kernel.cuh"
 #include "q8_quantiles.cuh"
+#include "q8_quant_kernel.cuh"
 
 namespace q8 {
 void build_dynamic_codebook(bool is_signed, float out[256]);
@@ -223,6 +224,23 @@ q8_status check_common(q8_dtype gdt, int32_t blocksize) {
 
 }  // namespace
 
+namespace {
+// Launch the TMA-pipelined quantizer (q8_quant_kernel.cuh): one persistent CTA per SM at most.
+template <int QTAB, bool kSigned, bool TW>
+q8_status launch_quant(const DeviceState* d, const float* code, const float* x, float* absmax, uint8_t* codes,
+                       int64_t n, cudaStream_t st) {
+    const auto fn = q8::quantize_tma_kernel<QTAB, kSigned, TW>;
+    cudaError_t e = q8::ensure_smem(reinterpret_cast<const void*>(fn), q8::kQtSmemBytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(quantizer)");
+    const int64_t nb = (n + q8::kBlock - 1) / q8::kBlock;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((nb + q8::kQNSub - 1) / q8::kQNSub, d->sms));
+    fn<<<grid, q8::kQNSub * q8::kQSubT, q8::kQtSmemBytes, st>>>(d->tabs, code, x, absmax, codes, n, nb);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "quantize_tma_kernel launch");
+    return Q8_OK;
+}
+}  // namespace
+
 cudaError_t q8::ensure_smem(const void* fn, int smem) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -366,12 +384,9 @@ q8_status q8_quantize_tensorwise(const float* code_dev, const float* x_dev, floa
     const int64_t n4 = (n / 4 + q8::kThreads - 1) / q8::kThreads;
     const unsigned grid_r = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(n4, 4 * d->sms)));
     q8::tensor_absmax_kernel<<<grid_r, q8::kThreads, 0, st>>>(x_dev, n, reinterpret_cast<unsigned int*>(absmax_dev));
-    const int64_t nb = (n + q8::kBlock - 1) / q8::kBlock;
-    static int occ = ctas_per_sm(reinterpret_cast<const void*>(q8::quantize_blockwise_kernel<true>));
-    q8::quantize_blockwise_kernel<true><<<static_cast<unsigned>(grid_for(d, occ, nb)), q8::kThreads, 0, st>>>(
-        code_dev, x_dev, absmax_dev, codes_dev, n, nb);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e, "quantize_tensorwise launch");
+    if (q8_status s = launch_quant<q8::QTAB_GENERIC, true, true>(d, code_dev, x_dev, absmax_dev, codes_dev, n, st);
+        s != Q8_OK)
+        return s;
     return ok();
 }
 
@@ -410,12 +425,10 @@ q8_status q8_quantize_blockwise(const float* code_dev, const float* x_dev, float
         return fail(Q8_ERR_INVALID, "misaligned buffer (x 16 B, codes 4 B)");
     DeviceState* d = nullptr;
     if (q8_status s = device_state(&d); s != Q8_OK) return s;
-    const int64_t nb = (n + q8::kBlock - 1) / q8::kBlock;
-    static int occ = ctas_per_sm(reinterpret_cast<const void*>(q8::quantize_blockwise_kernel<false>));
-    q8::quantize_blockwise_kernel<false><<<static_cast<unsigned>(grid_for(d, occ, nb)), q8::kThreads, 0,
-                                    static_cast<cudaStream_t>(stream)>>>(code_dev, x_dev, absmax_dev, codes_dev, n, nb);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e, "quantize_blockwise_kernel launch");
+    if (q8_status s = launch_quant<q8::QTAB_GENERIC, true, false>(d, code_dev, x_dev, absmax_dev, codes_dev, n,
+                                                                   static_cast<cudaStream_t>(stream));
+        s != Q8_OK)
+        return s;
     return ok();
 }
 
@@ -429,22 +442,11 @@ q8_status q8_quantize_blockwise_dynamic(int32_t is_signed, const float* x_dev, f
         return fail(Q8_ERR_INVALID, "misaligned buffer (x 16 B, codes 4 B)");
     DeviceState* d = nullptr;
     if (q8_status s = device_state(&d); s != Q8_OK) return s;
-    const int64_t nb = (n + q8::kBlock - 1) / q8::kBlock;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const void* fn = is_signed ? reinterpret_cast<const void*>(q8::quantize_blockwise_dynamic_kernel<true, 3>)
-                               : reinterpret_cast<const void*>(q8::quantize_blockwise_dynamic_kernel<false, 3>);
-    const int smem = q8::step_smem_bytes(1, q8::G_F32);
-    cudaError_t e = q8::ensure_smem(fn, smem);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((nb + 2) / 3, d->sms));
-    if (is_signed)
-        q8::quantize_blockwise_dynamic_kernel<true, 3><<<grid, 3 * q8::kQDynSubThreads, smem, st>>>(d->tabs, x_dev,
-                                                                                             absmax_dev, codes_dev, n, nb);
-    else
-        q8::quantize_blockwise_dynamic_kernel<false, 3><<<grid, 3 * q8::kQDynSubThreads, smem, st>>>(d->tabs, x_dev,
-                                                                                              absmax_dev, codes_dev, n, nb);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e, "quantize_blockwise_dynamic_kernel launch");
+    const q8_status s = is_signed
+                            ? launch_quant<q8::QTAB_BUILTIN, true, false>(d, nullptr, x_dev, absmax_dev, codes_dev, n, st)
+                            : launch_quant<q8::QTAB_BUILTIN, false, false>(d, nullptr, x_dev, absmax_dev, codes_dev, n, st);
+    if (s != Q8_OK) return s;
     return ok();
 }
 
@@ -711,7 +713,8 @@ int64_t q8_zero_signal_bytes(int32_t world, int32_t num_ctas) {
 
 q8_status q8_optim8bit_step_zero_fused(q8_kind kind, q8_dtype g_dtype, int32_t world, int32_t rank,
                                        const void* const* g_peers_host, float* const* p_peers_host,
-                                       uint32_t* const* sig_peers_host, uint8_t* s1, uint8_t* s2, float* absmax1,
+                                       uint32_t* const* sig_peers_host, float* p_multicast, uint8_t* s1, uint8_t* s2,
+                                       float* absmax1,
                                        float* absmax2, int64_t n_pad, int32_t blocksize, const q8_hparams* hp,
                                        int64_t step, uint32_t epoch, int32_t num_ctas, void* stream) {
     if (q8_status s = reject_layerwise(kind); s != Q8_OK) return s;
@@ -746,13 +749,18 @@ q8_status q8_optim8bit_step_zero_fused(q8_kind kind, q8_dtype g_dtype, int32_t w
     P.num_tensors = 1;
     P.block_start[0] = 0;
     P.total_blocks = P.block_start[1] = shard / q8::kBlock;
-    P.t[0] = q8::TensorDesc{t.p, nullptr, s1, s2, absmax1, absmax2, shard};
+    // this rank's own gradient shard is read through the TMA stages like the plain step's
+    const int64_t gsz = g_dtype == Q8_F32 ? 4 : 2;
+    P.t[0] = q8::TensorDesc{t.p, static_cast<const uint8_t*>(g_peers_host[rank]) + static_cast<int64_t>(rank) * shard * gsz,
+                            s1, s2, absmax1, absmax2, shard};
     std::memset(&P.z, 0, sizeof P.z);
     for (int r = 0; r < world; ++r) {
         P.z.g[r] = g_peers_host[r];
         P.z.p[r] = p_peers_host[r];
         P.z.sig[r] = sig_peers_host[r];
     }
+    if (p_multicast && !aligned(p_multicast, 16)) return fail(Q8_ERR_INVALID, "p_multicast not 16-byte aligned");
+    P.z.p_mc = p_multicast;
     P.z.off = static_cast<int64_t>(rank) * shard;
     P.z.world = world;
     P.z.rank = rank;

@@ -1,6 +1,6 @@
-// q8_codec.cuh -- the stand-alone block-wise codec kernels (a8) for a caller-provided
-// table: quantize (Eq.4) with the 8-step Eytzinger search and IEEE division,
-// dequantize.  Included by q8_api.cu only.
+// q8_codec.cuh -- the stand-alone block-wise codec kernels (a8) besides the quantizer
+// (q8_quant_kernel.cuh): dequantize, the tensor-wise absmax of Eq.3 and the non-finite
+// gradient count.  Included by q8_api.cu only.
 #pragma once
 
 #include "q8_kernels.cuh"
@@ -8,82 +8,6 @@
 namespace q8 {
 
 // ---------------------------------------------------------------------------- codec kernels
-
-// In-order rank of Eytzinger node i (1..255) of the perfect 8-level tree.
-__device__ __forceinline__ int eytzinger_rank_dev(int i) {
-    const int level = 31 - __clz(i);
-    const int pos = i - (1 << level);
-    return (2 * pos + 1) * (1 << (7 - level)) - 1;
-}
-
-// Stage a caller-provided ascending table and derive its Eytzinger thresholds
-// T_k = RD((Q_k + Q_{k+1}) / 2): __fadd_rd rounds the exact sum down, the halving is exact.
-__device__ __forceinline__ void stage_generic_table(const float* __restrict__ code, float* sQ, float* sT) {
-    const int tid = threadIdx.x;
-    sQ[tid] = code[tid];
-    __syncthreads();
-    if (tid >= 1) {
-        const int k = eytzinger_rank_dev(tid);
-        sT[tid] = __fmul_rn(__fadd_rd(sQ[k], sQ[k + 1]), 0.5f);
-    } else {
-        sT[0] = __int_as_float(0x7f800000);
-    }
-    __syncthreads();
-}
-
-// Block-wise quantization, Eq.4 -- a8.  IEEE division for y = x / N_b.
-// TW (tensor-wise, Eq.3): N = absmax[0], the maximum over the whole tensor computed by
-// tensor_absmax_kernel beforehand; no per-block reduction, absmax is not written.
-template <bool TW>
-__global__ void __launch_bounds__(kThreads) quantize_blockwise_kernel(const float* __restrict__ code,
-                                                                      const float* __restrict__ x,
-                                                                      float* __restrict__ absmax,
-                                                                      uint8_t* __restrict__ codes, int64_t n,
-                                                                      int64_t nblocks) {
-    __shared__ float sQ[256], sT[256];
-    __shared__ float red[2][kWarps];
-    stage_generic_table(code, sQ, sT);
-    const int tid = threadIdx.x;
-    int parity = 0;
-    for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x, parity ^= 1) {
-        const int64_t base = b * kBlock;
-        const bool full = base + kBlock <= n;
-        float v[kGroups][kVec];
-        float mx = 0.0f;
-#pragma unroll
-        for (int c = 0; c < kGroups; ++c) {
-            const int64_t i0 = base + c * (kThreads * kVec) + tid * kVec;
-            if (full) {
-                float4 xv = ld_stream_f4(x + i0);
-                v[c][0] = xv.x; v[c][1] = xv.y; v[c][2] = xv.z; v[c][3] = xv.w;
-            } else {
-#pragma unroll
-                for (int e = 0; e < kVec; ++e) v[c][e] = (i0 + e < n) ? x[i0 + e] : 0.0f;
-            }
-#pragma unroll
-            for (int e = 0; e < kVec; ++e) mx = fmaxf(mx, fabsf(v[c][e]));
-        }
-        const float N = TW ? absmax[0] : block_max(mx, red[parity]);
-#pragma unroll
-        for (int c = 0; c < kGroups; ++c) {
-            const int64_t i0 = base + c * (kThreads * kVec) + tid * kVec;
-            uint32_t o = 0u;
-#pragma unroll
-            for (int e = 0; e < kVec; ++e) {
-                const float y = (N > 0.0f) ? __fdiv_rn(v[c][e], N) : 0.0f;
-                o |= eytzinger_search(sT, y) << (8 * e);
-            }
-            if (full) {
-                st_stream_u32(codes + i0, o);
-            } else {
-#pragma unroll
-                for (int e = 0; e < kVec; ++e)
-                    if (i0 + e < n) codes[i0 + e] = static_cast<uint8_t>(o >> (8 * e));
-            }
-        }
-        if (!TW && tid == 0) absmax[b] = N;
-    }
-}
 
 // Tensor-wise absmax N = max |T| (Eq.3; the "reduction over the entire tensor" that
 // block-wise quantization avoids): per-CTA REDUX/shared reduction, then one atomicMax

@@ -143,6 +143,7 @@ struct ZeroParams {
     const void* g[kMaxWorld];
     float* p[kMaxWorld];
     uint32_t* sig[kMaxWorld];   // [2 phases][world][grid] uint32 flags (epochs)
+    float* p_mc;                // NVLS multicast address of the parameter buffers (NULL: W peer stores)
     int64_t off;                // first element of this rank's shard
     int world, rank;
     uint32_t epoch;             // this call's flag value (strictly increasing, >= 1)

@@ -119,10 +119,16 @@ class ZeroFusedOptimizer8bit:
     of a shard is the rank-order binary32 sum / world (reading Z1).
 
     num_ctas: CTAs per rank (0 = one per SM).  Ranks that share one GPU (tests) must use at most
-    SMs / world each so that every CTA of every rank can be resident."""
+    SMs / world each so that every CTA of every rank can be resident.
+
+    multicast: "auto" (default) allocates the gradient, parameter and signal buffers with torch's
+    symmetric memory when every rank has its own GPU and the node supports NVLS multicast (NVSwitch):
+    the peers' buffers come from its rendezvous instead of CUDA IPC, and the all-gather becomes one
+    multimem.st per 16 bytes through the switch (the kernel's p_multicast).  "off" keeps IPC peer
+    mappings and W peer stores; "on" requires multicast (raises otherwise)."""
 
     def __init__(self, n_params: int, kind: str = "adamw", grad_dtype=torch.bfloat16, device=None, group=None,
-                 num_ctas: int = 0, **hparams):
+                 num_ctas: int = 0, multicast: str = "auto", **hparams):
         if kind not in ("adam", "adamw", "momentum"):
             raise ValueError("the fused ZeRO step takes adam / adamw / momentum")
         self.group = group
@@ -134,9 +140,15 @@ class ZeroFusedOptimizer8bit:
         self.lo, self.hi = shard_range(self.n_pad, self.world, self.rank)
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.num_ctas = num_ctas
-        self.params = torch.zeros(self.n_pad, dtype=torch.float32, device=dev)
-        self.grads = torch.zeros(self.n_pad, dtype=grad_dtype, device=dev)
-        self.signal = torch.zeros(B.zero_signal_bytes(self.world, num_ctas), dtype=torch.uint8, device=dev)
+        self.p_mc = None
+        sig_bytes = B.zero_signal_bytes(self.world, num_ctas)
+        handles = self._symmetric(dev, grad_dtype, sig_bytes, group) if multicast != "off" else None
+        if handles is None and multicast == "on":
+            raise RuntimeError("NVLS multicast is not available (needs one GPU per rank on an NVSwitch node)")
+        if handles is None:
+            self.params = torch.zeros(self.n_pad, dtype=torch.float32, device=dev)
+            self.grads = torch.zeros(self.n_pad, dtype=grad_dtype, device=dev)
+            self.signal = torch.zeros(sig_bytes, dtype=torch.uint8, device=dev)
         shard = self.hi - self.lo
         two = kind != "momentum"
         self.s1 = torch.zeros(shard, dtype=torch.uint8, device=dev)
@@ -147,6 +159,14 @@ class ZeroFusedOptimizer8bit:
         self.t = 0
         self.epoch = 0
         torch.cuda.synchronize(dev)
+        if handles is not None:   # symmetric memory: peers' addresses and the multicast address
+            hg, hp, hs = handles
+            self._g, self._p, self._sig = list(hg.buffer_ptrs), list(hp.buffer_ptrs), list(hs.buffer_ptrs)
+            self.p_mc = int(hp.multicast_ptr)
+            self._peers = [[hg.get_buffer(r, (self.n_pad,), grad_dtype), hp.get_buffer(r, (self.n_pad,), torch.float32),
+                            hs.get_buffer(r, (sig_bytes,), torch.uint8)] for r in range(self.world)]
+            dist.barrier(group)
+            return
         if self.world > 1:
             self._peers = exchange_peer_tensors([self.grads, self.params, self.signal], group)
             dist.barrier(group)
@@ -155,6 +175,29 @@ class ZeroFusedOptimizer8bit:
         self._g = [pt[0].data_ptr() for pt in self._peers]
         self._p = [pt[1].data_ptr() for pt in self._peers]
         self._sig = [pt[2].data_ptr() for pt in self._peers]
+
+    def _symmetric(self, dev, grad_dtype, sig_bytes, group):
+        """Allocate grads / params / signal pad in torch symmetric memory and rendezvous them, if the
+        ranks have distinct GPUs and the node supports multicast; None otherwise."""
+        if self.world < 2 or not dist.is_initialized() or dist.get_backend(group) != "nccl":
+            return None
+        try:
+            import torch.distributed._symmetric_memory as symm
+            if not symm._SymmetricMemory.has_multicast_support(torch._C._autograd.DeviceType.CUDA, dev.index):
+                return None
+            grp = group if group is not None else dist.group.WORLD
+            bufs = [symm.empty(self.n_pad, dtype=grad_dtype, device=dev),
+                    symm.empty(self.n_pad, dtype=torch.float32, device=dev),
+                    symm.empty(sig_bytes, dtype=torch.uint8, device=dev)]
+            for t in bufs:
+                t.zero_()
+            hs = [symm.rendezvous(t, grp) for t in bufs]
+            if not int(getattr(hs[1], "multicast_ptr", 0) or 0):
+                return None
+        except Exception:  # noqa: BLE001  (no symmetric-memory backend / no multicast on this node)
+            return None
+        self.grads, self.params, self.signal = bufs
+        return hs
 
     @property
     def p_shard(self) -> torch.Tensor:
@@ -166,4 +209,4 @@ class ZeroFusedOptimizer8bit:
         self.epoch += 1
         B.optim8bit_step_zero_fused(self.kind, self.world, self.rank, self._g, self._p, self._sig, self.s1, self.s2,
                                     self.absmax1, self.absmax2, self.n_pad, self.grads.dtype, step=self.t,
-                                    epoch=self.epoch, num_ctas=self.num_ctas, hp=self.hp)
+                                    epoch=self.epoch, num_ctas=self.num_ctas, hp=self.hp, p_multicast=self.p_mc)

@@ -16,17 +16,27 @@ import synth  # noqa: E402
 def main():
     out_dir, n, kind, gdt, steps, ctas = sys.argv[1], int(sys.argv[2]), sys.argv[3], sys.argv[4], int(sys.argv[5]), \
         int(sys.argv[6])
-    torch.cuda.set_device(0)
-    dist.init_process_group("gloo")
+    mode = sys.argv[7] if len(sys.argv) > 7 else "shared"
+    if mode == "nvls":   # one GPU per rank, NCCL, symmetric memory with NVLS multicast (required)
+        local = int(os.environ["LOCAL_RANK"])
+        dev = torch.device("cuda", local)
+        torch.cuda.set_device(dev)
+        dist.init_process_group("nccl", device_id=dev)
+    else:                # every rank on cuda:0, gloo for the host exchange, CUDA IPC peer mappings
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        dist.init_process_group("gloo")
     rank = dist.get_rank()
     hp = dict(synth.HPARAMS[kind])
-    zo = q8.ZeroFusedOptimizer8bit(n, kind=kind, grad_dtype=getattr(torch, gdt), device="cuda:0", num_ctas=ctas, **hp)
-    zo.params[:n] = synth.params(n, seed=3).cuda()
+    zo = q8.ZeroFusedOptimizer8bit(n, kind=kind, grad_dtype=getattr(torch, gdt), device=dev, num_ctas=ctas,
+                                   multicast="on" if mode == "nvls" else "off", **hp)
+    assert (zo.p_mc is not None) == (mode == "nvls")
+    zo.params[:n] = synth.params(n, seed=3).to(dev)
     torch.cuda.synchronize()
     dist.barrier()
     for t in range(1, steps + 1):
         zo.grads.zero_()
-        zo.grads[:n] = synth.grads(n, step=t, seed=50 + rank, dtype=gdt).cuda()
+        zo.grads[:n] = synth.grads(n, step=t, seed=50 + rank, dtype=gdt).to(dev)
         torch.cuda.synchronize()
         dist.barrier()          # (a real trainer needs no host barrier: the kernel's flags order the ranks)
         zo.step()

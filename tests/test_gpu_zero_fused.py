@@ -43,14 +43,31 @@ def test_single_rank_equals_plain_step(kind, gdt):
     assert torch.count_nonzero(zo.params[n:]) == 0
 
 
-@pytest.mark.parametrize("kind,gdt", [("adamw", "bfloat16"), ("momentum", "float32")])
-def test_two_ranks_sharing_one_gpu(tmp_path, kind, gdt):
-    n, steps, world = 13 * 2048 + 777, 3, 2
+def _run_ranks(tmp_path, kind, gdt, world, mode, ctas):
+    n, steps = 13 * 2048 + 777, 3
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(world),
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + (os.getpid() % 300)),
-           os.path.join(ROOT, "tests", "_zero_fused_worker.py"), str(tmp_path), str(n), kind, gdt, str(steps), "74"]
+           os.path.join(ROOT, "tests", "_zero_fused_worker.py"), str(tmp_path), str(n), kind, gdt, str(steps),
+           str(ctas), mode]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    _check_against_oracle(tmp_path, kind, gdt, world, n, steps)
+
+
+@pytest.mark.parametrize("kind,gdt", [("adamw", "bfloat16"), ("momentum", "float32")])
+def test_two_ranks_sharing_one_gpu(tmp_path, kind, gdt):
+    _run_ranks(tmp_path, kind, gdt, 2, "shared", 74)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="NVLS multicast needs one GPU per rank (>= 2 GPUs)")
+@pytest.mark.parametrize("kind,gdt", [("adamw", "bfloat16"), ("adam", "float16")])
+def test_nvls_multicast_all_gather(tmp_path, kind, gdt):
+    """One rank per GPU (NCCL), buffers in torch symmetric memory, the all-gather as multimem.st
+    through NVSwitch: bit-exact against the oracle like the peer-store path (reading Z1)."""
+    _run_ranks(tmp_path, kind, gdt, min(4, torch.cuda.device_count()), "nvls", 0)
+
+
+def _check_against_oracle(tmp_path, kind, gdt, world, n, steps):
     hp = dict(synth.HPARAMS[kind])
     B = 2048
     unit = world * B
