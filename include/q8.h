@@ -233,7 +233,7 @@ q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_t
 
 /* Bytes of workspace q8_optim8bit_step_layerwise needs for these tensors (host function): 4 per
  * tensor (rounded up to 16) + 128 per 2048-block of the largest launch chunk (binary64 partial
- * norms per warp).  -1 on bad input. */
+ * norms per warp) + 16 (the grid barrier of the one-launch LARS step).  -1 on bad input. */
 int64_t q8_layerwise_workspace_bytes(const q8_tensor* tensors_host, int32_t num_tensors);
 
 /* Fused ZeRO-1 step over peer memory: ONE kernel per rank does

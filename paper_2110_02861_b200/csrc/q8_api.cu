@@ -634,7 +634,8 @@ int64_t q8_layerwise_workspace_bytes(const q8_tensor* tensors_host, int32_t num_
     if (num_tensors < 0 || (num_tensors > 0 && !tensors_host)) return -1;
     for (int32_t i = 0; i < num_tensors; ++i)
         if (tensors_host[i].n < 0) return -1;
-    return lw_scale_bytes(num_tensors) + 16 * q8::kNormSlots * lw_partial_blocks(tensors_host, num_tensors);
+    // + 16 B: the grid barrier of the one-launch LARS step
+    return lw_scale_bytes(num_tensors) + 16 * q8::kNormSlots * lw_partial_blocks(tensors_host, num_tensors) + 16;
 }
 
 q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_tensor* tensors_host,
@@ -663,6 +664,10 @@ q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_t
     double2* partial = reinterpret_cast<double2*>(static_cast<uint8_t*>(workspace_dev) + lw_scale_bytes(num_tensors));
     static thread_local q8::StepParams<kLwChunk> P;
     P.s = make_scalars(hp, step, kind);
+    P.lw.lr = hp->lr;
+    P.lw.eta = trust_coefficient;
+    P.lw.wd = hp->weight_decay;
+    P.lw.gbar = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(workspace_dev) + need - 16);
     const q8::LaunchCtx ctx{d->tabs, d->sms, static_cast<cudaStream_t>(stream), q8::SEARCH_BUCKET, 0, 0};
     for (int32_t c = 0; c < num_tensors; c += kLwChunk) {
         // every tensor of the chunk keeps its slot (empty ones have no blocks) so that

@@ -149,7 +149,17 @@ struct ZeroParams {
     uint32_t epoch;             // this call's flag value (strictly increasing, >= 1)
     float invw;                 // 1/world (exact when pow2)
     int pow2;
+    int64_t pad_;               // keeps the size a multiple of 16 B (the fields after it stay 16-B aligned)
 };
+static_assert(sizeof(ZeroParams) % 16 == 0, "ZeroParams keeps the step parameters 16-byte aligned");
+
+// LARS in ONE cooperative launch (MODE_LARSF): norms pass, grid barrier, per-tensor scales, grid
+// barrier, fused step.  gbar: [count, generation] of the grid barrier (count 0 on entry).
+struct LayerwiseFused {
+    double lr, eta, wd;
+    unsigned int* gbar;
+};
+static_assert(sizeof(LayerwiseFused) % 16 == 0, "keeps the step parameters 16-byte aligned");
 
 template <int MAXT>
 struct StepParams {
@@ -157,6 +167,7 @@ struct StepParams {
     DeviceStep ds;                  // multi-tensor plans only (ds.step NULL otherwise)
     const float* scale;             // LAMB / LARS: per-tensor trust scale RN(lr*ratio) (L1-L3)
     double2* partial;               // LAMB norms pass: per-block (sum w^2, sum u^2)
+    LayerwiseFused lw;              // LARS one-launch mode only
     ZeroParams z;                   // fused ZeRO-1 mode only
     int num_tensors;
     int64_t total_blocks;

@@ -87,6 +87,28 @@ cudaError_t launch_layerwise_t(const StepParams<kMultiMaxT>& P, const LaunchCtx&
         return cudaGetLastError();
     }
     cudaError_t e;
+    if constexpr (KIND == KIND_LARS) {
+        // one cooperative launch: norms, grid barrier, scales, grid barrier, step (MODE_LARSF)
+        const auto fn = optim8bit_step_kernel<KIND, G, kMultiMaxT, SEARCH_BUCKET, NS, SUBT, MODE_LARSF>;
+        const int smem = step_smem_bytes(NS, G);
+        e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
+        if (e != cudaSuccess) return e;
+        e = cudaMemsetAsync(P.lw.gbar, 0, 2 * sizeof(unsigned int), ctx.stream);
+        if (e != cudaSuccess) return e;
+        int64_t grid = (P.total_blocks + NS - 1) / NS;
+        if (grid > ctx.sms) grid = ctx.sms;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(grid));
+        cfg.blockDim = dim3(NS * SUBT);
+        cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+        cfg.stream = ctx.stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, fn, P, ctx.tabs);
+    }
     if constexpr (KIND == KIND_LAMB) {
         e = persistent(optim8bit_step_kernel<KIND, G, kMultiMaxT, SEARCH_BUCKET, NS, SUBT, MODE_NORMS>, NS, SUBT,
                        P.total_blocks, ctx, P, ctx.tabs);
