@@ -175,6 +175,12 @@ struct StepParams {
     TensorDesc t[MAXT];
 };
 
+// The gradient of tensor ti of a launch.
+template <int MAXT>
+__device__ __forceinline__ const void* grad_of(const StepParams<MAXT>&, const TensorDesc& T, int) {
+    return T.g;
+}
+
 // ---------------------------------------------------------------------------- loads
 
 __device__ __forceinline__ float4 ld_stream_f4(const float* p) { return __ldcs(reinterpret_cast<const float4*>(p)); }

@@ -1,0 +1,3 @@
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 300 python tools/probe_launch.py
+bash tools/gpu_sanitize_r2.sh
