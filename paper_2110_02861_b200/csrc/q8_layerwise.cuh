@@ -13,6 +13,8 @@
 //                           tensor's scale a = RN(lr * ratio) (binary64 ratio, L3)
 //   3. optim8bit_step_kernel<KIND_LAMB / KIND_LARS>  the fused step with the tensor's scale
 // HBM traffic per parameter with bf16 grads: LAMB 8 B (pass 1) + 14 B (pass 3); LARS 6 B + 12 B.
+// LAMB's pass 1 keeps two blocks in flight per sub-block (q8_step_kernel.cuh, stage_part_b).  LARS can
+// also run as one cooperative launch (MODE_LARSF in q8_step_kernel.cuh, Q8_LARS_ONE_LAUNCH=1).
 #pragma once
 
 #include "q8_kernels.cuh"

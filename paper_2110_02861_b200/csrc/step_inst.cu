@@ -1,6 +1,7 @@
 // step_inst.cu -- instantiates and launches the fused step kernels for ONE gradient dtype
 // (Q8_GDT = 0 fp32, 1 fp16, 2 bf16); build.py compiles this file once per dtype in parallel.
 #include <algorithm>
+#include <cstdlib>
 
 #include "q8_launch.h"
 #include "q8_layerwise.cuh"
@@ -87,8 +88,15 @@ cudaError_t launch_layerwise_t(const StepParams<kMultiMaxT>& P, const LaunchCtx&
         return cudaGetLastError();
     }
     cudaError_t e;
-    if constexpr (KIND == KIND_LARS) {
-        // one cooperative launch: norms, grid barrier, scales, grid barrier, step (MODE_LARSF)
+    // LARS as ONE cooperative launch (MODE_LARSF: norms, grid barrier, scales, grid barrier, step) when
+    // Q8_LARS_ONE_LAUNCH=1.  Measured slower than the three launches below on ResNet-50 (0.121 vs
+    // 0.110 ms): the persistent 16-warp CTAs hide the norms pass's load latency worse
+    // than the many small CTAs of lars_norms_kernel, and each grid barrier adds a tail.
+    static const bool one_launch = [] {
+        const char* v = std::getenv("Q8_LARS_ONE_LAUNCH");
+        return v && std::atoi(v) == 1;
+    }();
+    if constexpr (KIND == KIND_LARS) if (one_launch) {
         const auto fn = optim8bit_step_kernel<KIND, G, kMultiMaxT, SEARCH_BUCKET, NS, SUBT, MODE_LARSF>;
         const int smem = step_smem_bytes(NS, G);
         e = ensure_smem(reinterpret_cast<const void*>(fn), smem);

@@ -181,3 +181,18 @@ def test_layerwise_random_sweep(q8, i):
         assert ulps.max() <= 1, (got, exp)
         _assert_equal(kind, ents, refs)
         t += 1
+
+
+def test_lars_one_launch_variant():
+    """The one-launch LARS (Q8_LARS_ONE_LAUNCH=1: norms, grid barrier, scales, grid barrier, step in one
+    cooperative kernel) passes the same teacher-forced parity tests as the default three launches."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, Q8_LARS_ONE_LAUNCH="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", os.path.abspath(__file__),
+                        "-k", "lars and not one_launch"], capture_output=True, text=True, env=env, cwd=root,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
