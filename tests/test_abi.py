@@ -10,6 +10,7 @@ import pytest
 import torch
 
 import oracle
+import synth
 import paper_2110_02861_b200 as q8
 from paper_2110_02861_b200 import _binding as B
 
@@ -183,3 +184,52 @@ def test_binding_rejects_bad_tensors_before_the_c_call():
         q8.count_nonfinite(torch.zeros(8, dtype=torch.int32))
     with pytest.raises(ValueError, match="257"):
         q8.create_quantile_codebook(torch.zeros(10))
+
+
+def test_plan_validation_without_device():
+    """q8_plan_*: argument validation happens before any CUDA call (kind, dtype, block size, tensor
+    descriptors of both state widths, NULLs); the plan calls reject NULL plans."""
+    arr = (B.TensorDesc * 2)()
+    arr[0] = B.TensorDesc(FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, 100)
+    arr[1] = B.TensorDesc(FAKE, FAKE + 2, FAKE, FAKE, FAKE, FAKE, 100)   # misaligned gradient
+    a32 = (B.TensorDesc32 * 1)()
+    a32[0] = B.TensorDesc32(FAKE, FAKE, FAKE, 0, 100)                  # Adam needs r
+    out = ctypes.c_void_p()
+    create = B.lib.q8_plan_create
+    assert create(B.Q8_ADAM, B.Q8_BF16, arr, 2, None, 0, 2048, ctypes.byref(out)) == B.Q8_ERR_INVALID
+    assert "tensor 1" in B.lib.q8_last_error().decode()
+    assert create(B.Q8_ADAM, B.Q8_BF16, arr, 1, a32, 1, 2048, ctypes.byref(out)) == B.Q8_ERR_INVALID
+    assert "tensor 1" in B.lib.q8_last_error().decode()
+    assert create(B.Q8_LAMB, B.Q8_BF16, arr, 1, None, 0, 2048, ctypes.byref(out)) == B.Q8_ERR_INVALID
+    assert create(B.Q8_ADAM, 9, arr, 1, None, 0, 2048, ctypes.byref(out)) == B.Q8_ERR_INVALID
+    assert create(B.Q8_ADAM, B.Q8_BF16, arr, 1, None, 0, 4096, ctypes.byref(out)) == B.Q8_ERR_UNSUPPORTED
+    assert create(B.Q8_ADAM, B.Q8_BF16, None, 1, None, 0, 2048, ctypes.byref(out)) == B.Q8_ERR_INVALID
+    assert create(B.Q8_ADAM, B.Q8_BF16, arr, 1, None, 0, 2048, None) == B.Q8_ERR_INVALID
+    assert out.value is None
+    g = (ctypes.c_void_p * 1)(FAKE)
+    assert B.lib.q8_plan_set_grads(None, g, 1) == B.Q8_ERR_INVALID
+    assert B.lib.q8_plan_step(None, ctypes.byref(_hp()), 1, None) == B.Q8_ERR_INVALID
+    assert B.lib.q8_plan_step_device(None, ctypes.byref(_hp()), FAKE, None) == B.Q8_ERR_INVALID
+    B.lib.q8_plan_destroy(None)
+
+
+@pytest.mark.parametrize("kind,hpkey", [("adam", "adam"), ("adamw", "adamw"), ("lamb", "lamb")])
+def test_host_step_scalars_follow_g8(kind, hpkey):
+    """q8_step_scalars (host): the G8-G10 scalars each rounded once from binary64 -- checked here
+    against numpy binary64 arithmetic for several steps (the device copy is compared with these on the
+    GPU, tests/test_gpu_plan.py)."""
+    h = dict(synth.HPARAMS[hpkey])
+    h.pop("trust_coefficient", None)
+    hp = q8.hparams(**h)
+    for t in (1, 2, 10, 1000, 123456):
+        s = q8.step_scalars(kind, hp, t).numpy()
+        bc1 = 1.0 - np.power(np.float64(h["beta1"]), t)
+        bc2 = 1.0 - np.power(np.float64(h["beta2"]), t)
+        if kind == "lamb":
+            step_size = np.sqrt(bc2) / bc1
+        else:
+            step_size = h["lr"] * np.sqrt(bc2) / bc1
+        assert s[5] == np.float32(step_size)
+        assert s[6] == np.float32(h["eps"] * np.sqrt(bc2))
+        assert s[8] == np.float32(1.0 - h["lr"] * h["weight_decay"])
+        assert s[3] == np.float32(1.0 - h["beta1"]) and s[4] == np.float32(1.0 - h["beta2"])
