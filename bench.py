@@ -801,7 +801,7 @@ def main_layerwise(args, cfg, q8, world, rank, local, dev):
         return q8.TensorList(ents)
 
     tls = [tlist(g) for g in gpool]
-    ws = torch.empty(q8.layerwise_workspace_bytes(tls[0]), dtype=torch.uint8, device=dev)
+    ws = torch.zeros(q8.layerwise_workspace_bytes(tls[0]), dtype=torch.uint8, device=dev)
     hpo = q8.hparams(**hp)
     step = 0
 

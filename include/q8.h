@@ -217,11 +217,14 @@ q8_status q8_optim32bit_step_multi(q8_kind kind, q8_dtype g_dtype, const q8_tens
  * Norms are over the whole tensor, of the PRE-update w (and of u from the fp32 post-update
  * states), accumulated in binary64; the per-tensor scale is rounded once to fp32 (L3).  States
  * are dequantized / requantized block-wise exactly as in q8_optim8bit_step.
- * Three stream-ordered launches per chunk of Q8_MAX_TENSORS_PER_LAUNCH tensors: a norms pass
- * (reads w, g and, LAMB, the states), a per-tensor scale pass, the fused step.
+ * Stream-ordered launches per chunk of Q8_MAX_TENSORS_PER_LAUNCH tensors: LAMB a norms pass (reads
+ * w, g and the states), a per-tensor scale pass, the fused step; LARS a norms pass that also computes
+ * the scales (the CTA that finishes a tensor's last block sums its partials), then the fused step as a
+ * programmatic dependent launch (it stages its tables while the norms pass drains).
  *   workspace_dev  device scratch of at least q8_layerwise_workspace_bytes(tensors, n) bytes,
- *                  16-B aligned, caller-owned; must not be used by another call until this one
- *                  completes on `stream`.  On completion its first 4*num_tensors bytes hold each
+ *                  16-B aligned, caller-owned, ZERO-FILLED before its first use (it holds block
+ *                  counters that every call leaves at zero again); must not be used by another call
+ *                  until this one completes on `stream`.  On completion its first 4*num_tensors bytes hold each
  *                  tensor's fp32 scale (float scale[i] for tensors_host[i]; lr for empty tensors)
  *                  -- the trust ratio times lr, a diagnostic output.
  * Other arguments, alignment and errors as q8_optim8bit_step_multi; INVALID also for a kind
@@ -233,7 +236,8 @@ q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_t
 
 /* Bytes of workspace q8_optim8bit_step_layerwise needs for these tensors (host function): 4 per
  * tensor (rounded up to 16) + 128 per 2048-block of the largest launch chunk (binary64 partial
- * norms per warp) + 16 (the grid barrier of the one-launch LARS step).  -1 on bad input. */
+ * norms per warp) + 4 * Q8_MAX_TENSORS_PER_LAUNCH (per-tensor block counters of the LARS norms pass)
+ * + 16 (the grid barrier of the one-launch LARS step).  -1 on bad input. */
 int64_t q8_layerwise_workspace_bytes(const q8_tensor* tensors_host, int32_t num_tensors);
 
 /* Fused ZeRO-1 step over peer memory: ONE kernel per rank does

@@ -386,7 +386,7 @@ def optim8bit_step_layerwise(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1
     if need < 0:
         raise ValueError("invalid tensor list")
     if workspace is None or workspace.numel() < need:
-        workspace = torch.empty(need, dtype=torch.uint8, device=tl.device)
+        workspace = torch.zeros(need, dtype=torch.uint8, device=tl.device)  # zero-filled (q8.h)
     if hp is None:
         hp = hparams(lr, beta1, beta2, eps, weight_decay, bias_correction)
     with _on(tl.device):

@@ -614,6 +614,7 @@ constexpr int kLwChunk = Q8_MAX_TENSORS_PER_LAUNCH;
 
 // Workspace layout: float scale[num_tensors] (rounded up to 16 B), then double2 partial[] sized
 // for the largest chunk of kLwChunk consecutive tensors.
+constexpr int64_t kLwCountBytes = 4 * kLwChunk;  // zero between calls (the norms pass resets them)
 int64_t lw_scale_bytes(int32_t num_tensors) { return (static_cast<int64_t>(num_tensors) * 4 + 15) / 16 * 16; }
 
 int64_t lw_partial_blocks(const q8_tensor* t, int32_t num_tensors) {
@@ -634,8 +635,10 @@ int64_t q8_layerwise_workspace_bytes(const q8_tensor* tensors_host, int32_t num_
     if (num_tensors < 0 || (num_tensors > 0 && !tensors_host)) return -1;
     for (int32_t i = 0; i < num_tensors; ++i)
         if (tensors_host[i].n < 0) return -1;
-    // + 16 B: the grid barrier of the one-launch LARS step
-    return lw_scale_bytes(num_tensors) + 16 * q8::kNormSlots * lw_partial_blocks(tensors_host, num_tensors) + 16;
+    // + the per-tensor block counters of the LARS norms pass (one launch chunk), + 16 B: the grid barrier
+    // of the one-launch LARS step
+    return lw_scale_bytes(num_tensors) + 16 * q8::kNormSlots * lw_partial_blocks(tensors_host, num_tensors) +
+           kLwCountBytes + 16;
 }
 
 q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_tensor* tensors_host,
@@ -668,6 +671,7 @@ q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_t
     P.lw.eta = trust_coefficient;
     P.lw.wd = hp->weight_decay;
     P.lw.gbar = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(workspace_dev) + need - 16);
+    unsigned int* count = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(workspace_dev) + need - 16 - kLwCountBytes);
     const q8::LaunchCtx ctx{d->tabs, d->sms, static_cast<cudaStream_t>(stream), q8::SEARCH_BUCKET, 0, 0};
     for (int32_t c = 0; c < num_tensors; c += kLwChunk) {
         // every tensor of the chunk keeps its slot (empty ones have no blocks) so that
@@ -687,11 +691,11 @@ q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_t
         P.partial = partial;
         cudaError_t e = cudaErrorInvalidValue;
         switch (g_dtype) {
-            case Q8_F32: e = q8::launch_layerwise_g0(kind, P, ctx, partial, scale + c, hp->lr, trust_coefficient,
+            case Q8_F32: e = q8::launch_layerwise_g0(kind, P, ctx, partial, scale + c, count, hp->lr, trust_coefficient,
                                                      hp->weight_decay); break;
-            case Q8_F16: e = q8::launch_layerwise_g1(kind, P, ctx, partial, scale + c, hp->lr, trust_coefficient,
+            case Q8_F16: e = q8::launch_layerwise_g1(kind, P, ctx, partial, scale + c, count, hp->lr, trust_coefficient,
                                                      hp->weight_decay); break;
-            case Q8_BF16: e = q8::launch_layerwise_g2(kind, P, ctx, partial, scale + c, hp->lr, trust_coefficient,
+            case Q8_BF16: e = q8::launch_layerwise_g2(kind, P, ctx, partial, scale + c, count, hp->lr, trust_coefficient,
                                                       hp->weight_decay); break;
         }
         if (e != cudaSuccess) return cuda_fail(e, "layer-wise step launch");

@@ -30,13 +30,14 @@ cudaError_t launch_step_g2(int kind, const StepParams<1>* single, const StepPara
                            const LaunchCtx& ctx);
 
 // Layer-wise step (LAMB / LARS) for gradient dtype g<N>: norms pass, per-tensor scale pass
-// (writes scale[0 .. P.num_tensors)), fused step; partial holds P.total_blocks entries.
+// (writes scale[0 .. P.num_tensors)), fused step; partial holds P.total_blocks entries; count holds
+// P.num_tensors block counters, zero on entry and on return (LARS: the scales come from its norms pass).
 cudaError_t launch_layerwise_g0(int kind, const StepParams<kMultiMaxT>& P, const LaunchCtx& ctx, double2* partial,
-                                float* scale, double lr, double eta, double wd);
+                                float* scale, unsigned int* count, double lr, double eta, double wd);
 cudaError_t launch_layerwise_g1(int kind, const StepParams<kMultiMaxT>& P, const LaunchCtx& ctx, double2* partial,
-                                float* scale, double lr, double eta, double wd);
+                                float* scale, unsigned int* count, double lr, double eta, double wd);
 cudaError_t launch_layerwise_g2(int kind, const StepParams<kMultiMaxT>& P, const LaunchCtx& ctx, double2* partial,
-                                float* scale, double lr, double eta, double wd);
+                                float* scale, unsigned int* count, double lr, double eta, double wd);
 
 // Fused ZeRO-1 step (MODE_ZERO) for gradient dtype g<N> with exactly `grid` CTAs (identical on
 // every rank: the cross-rank barrier pairs CTA i with CTA i).

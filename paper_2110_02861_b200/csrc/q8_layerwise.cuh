@@ -3,7 +3,8 @@
 // DESIGN.md section 3.
 //
 // A layer-wise step needs per-tensor norms before any parameter can move, so it is three
-// stream-ordered launches per chunk of <= 384 tensors:
+// stream-ordered launches per chunk of <= 384 tensors (LARS: two -- its norms pass also computes the
+// scales, lars_norms_kernel below):
 //   1. norms pass           per 2048-block partial sums (binary64) of w^2 and of x^2, where
 //                           x = u (LAMB: the update direction from the fp32 post-update states,
 //                           computed exactly as pass 3 computes it -- the fused step kernel in
@@ -28,15 +29,78 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
     return v;
 }
 
-// LARS norms pass: per-block binary64 partial sums of w^2 and g^2 (reads p and g only).  LAMB's
-// norms pass needs the full dequantize + update and runs in the fused step kernel's MODE_NORMS.
-template <int GDT, int MAXT>
-__global__ void __launch_bounds__(kThreads) lars_norms_kernel(const __grid_constant__ StepParams<MAXT> P) {
-    static_assert(kWarps == kNormSlots, "one partial slot per warp");
+// LARS norms pass with the per-tensor scales folded in (two launches per LARS step instead of three).
+// CTA q takes the contiguous block range [q*B/Q, (q+1)*B/Q) of the launch.  Per block: binary64 sums
+// of w^2 and g^2 (warp butterflies, then the 8 warps in order: ONE partial per block, partial[block]).
+// When the range leaves a tensor (and at its end) thread 0 adds the number of that tensor's blocks it
+// summed to the tensor's counter (count[t], zero on entry); the CTA that completes a tensor's count
+// sums its partials in a fixed order (thread-strided over blocks, warp butterfly, warps in order --
+// reading L3: any fixed order) and writes scale[t] = RN(lr * eta ||w|| / (||g|| + wd ||w||)) (lr when
+// a norm is 0, L2), then resets count[t] to 0.  Empty tensors (no blocks) get scale lr.  The kernel
+// lets the step launch early (programmatic dependent launch): the step stages its tables and first
+// blocks while this pass drains, and waits for it (griddepcontrol.wait) before it reads any scale.
+template <int MAXT>
+__device__ __forceinline__ void lars_count_tensor(const StepParams<MAXT>& P, int ti, unsigned int seg,
+                                                  unsigned int* __restrict__ count, float* __restrict__ scale,
+                                                  double (*red)[kWarps], int* last) {
     const int tid = threadIdx.x;
-    int ti = 0;
-    for (int64_t gb = blockIdx.x; gb < P.total_blocks; gb += gridDim.x) {
-        ti = find_tensor<MAXT>(P, gb, ti);
+    if (tid == 0) {
+        __threadfence();  // this CTA's partials of ti (all written by thread 0) before they are counted
+        const unsigned int nb = static_cast<unsigned int>(P.block_start[ti + 1] - P.block_start[ti]);
+        *last = atomicAdd(count + ti, seg) + seg == nb;
+    }
+    __syncthreads();
+    if (!*last) return;
+    __threadfence();
+    double aw = 0.0, ag = 0.0;
+    for (int64_t b = P.block_start[ti] + tid; b < P.block_start[ti + 1]; b += kThreads) {
+        const double2 v = __ldcg(P.partial + b);
+        aw += v.x;
+        ag += v.y;
+    }
+    aw = warp_sum_f64(aw);
+    ag = warp_sum_f64(ag);
+    if ((tid & 31) == 0) {
+        red[0][tid >> 5] = aw;
+        red[1][tid >> 5] = ag;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        aw = ag = 0.0;
+        for (int k = 0; k < kWarps; ++k) {
+            aw += red[0][k];
+            ag += red[1][k];
+        }
+        const double wn = sqrt(aw), gn = sqrt(ag);
+        double f = 1.0;
+        if (wn > 0.0 && gn > 0.0) f = P.lw.eta * wn / (gn + P.lw.wd * wn);
+        scale[ti] = static_cast<float>(P.lw.lr * f);
+        count[ti] = 0u;
+    }
+    __syncthreads();  // red and *last are free again
+}
+
+template <int GDT, int MAXT>
+__global__ void __launch_bounds__(kThreads) lars_norms_kernel(const __grid_constant__ StepParams<MAXT> P,
+                                                              unsigned int* __restrict__ count,
+                                                              float* __restrict__ scale) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __shared__ double red[2][2][kWarps];  // [block parity][w, g][warp]
+    __shared__ int last;
+    const int tid = threadIdx.x;
+    for (int t = blockIdx.x * kThreads + tid; t < P.num_tensors; t += gridDim.x * kThreads)
+        if (P.block_start[t + 1] == P.block_start[t]) scale[t] = static_cast<float>(P.lw.lr);
+    const int64_t gb0 = static_cast<int64_t>(blockIdx.x) * P.total_blocks / gridDim.x;
+    const int64_t gb1 = static_cast<int64_t>(blockIdx.x + 1) * P.total_blocks / gridDim.x;
+    if (gb0 >= gb1) return;
+    int ti = find_tensor<MAXT>(P, gb0, 0);
+    unsigned int seg = 0;  // blocks of tensor ti summed by this CTA
+    for (int64_t gb = gb0; gb < gb1; ++gb) {
+        if (gb >= P.block_start[ti + 1]) {
+            lars_count_tensor<MAXT>(P, ti, seg, count, scale, red[0], &last);
+            ti = find_tensor<MAXT>(P, gb, ti);
+            seg = 0;
+        }
         const TensorDesc& T = P.t[ti];
         const int64_t base = (gb - P.block_start[ti]) * kBlock;
         const bool full = base + kBlock <= T.n;
@@ -65,8 +129,24 @@ __global__ void __launch_bounds__(kThreads) lars_norms_kernel(const __grid_const
         }
         sw = warp_sum_f64(sw);
         sg = warp_sum_f64(sg);
-        if ((tid & 31) == 0) P.partial[gb * kNormSlots + (tid >> 5)] = make_double2(sw, sg);
+        const int par = static_cast<int>(gb & 1);  // double-buffered: one barrier per block
+        if ((tid & 31) == 0) {
+            red[par][0][tid >> 5] = sw;
+            red[par][1][tid >> 5] = sg;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double a = 0.0, b = 0.0;
+#pragma unroll
+            for (int k = 0; k < kWarps; ++k) {
+                a += red[par][0][k];
+                b += red[par][1][k];
+            }
+            P.partial[gb] = make_double2(a, b);
+        }
+        ++seg;
     }
+    lars_count_tensor<MAXT>(P, ti, seg, count, scale, red[0], &last);
 }
 
 // One CTA (kThreads) per tensor of the launch: ||w|| and ||x|| from its per-warp block partials

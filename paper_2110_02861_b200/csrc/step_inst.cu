@@ -25,6 +25,29 @@ cudaError_t persistent(Kern fn, int nsub, int subt, int64_t work_blocks, const L
     return cudaGetLastError();
 }
 
+// The same launch as a programmatic dependent launch: the kernel may start while the previous kernel on
+// the stream drains (it must execute griddepcontrol.wait before consuming that kernel's results).
+template <typename... KArgs, typename... Args>
+cudaError_t persistent_pdl(void (*fn)(KArgs...), int nsub, int subt, int64_t work_blocks, const LaunchCtx& ctx,
+                           const Args&... args) {
+    const int smem = step_smem_bytes(nsub, Q8_GDT);
+    cudaError_t e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
+    if (e != cudaSuccess) return e;
+    int64_t grid = (work_blocks + nsub - 1) / nsub;
+    if (grid > ctx.sms) grid = ctx.sms;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(nsub * subt);
+    cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+    cfg.stream = ctx.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fn, args...);
+}
+
 // Sub-block size: 128 threads x 16 elements for 16-bit gradients (4 sub-blocks, 16 warps per
 // SM: the per-block overhead is amortized over more elements), 256 x 8 for fp32 gradients (their
 // 20 KB stages allow only 3 sub-blocks, so more warps per sub-block).  Q8_SUBT overrides.
@@ -78,7 +101,7 @@ cudaError_t launch_any(int kind, const StepParams<MAXT>& P, const LaunchCtx& ctx
 // Layer-wise kinds (LAMB, LARS): norms -> per-tensor scale -> fused step, default configuration.
 template <int KIND>
 cudaError_t launch_layerwise_t(const StepParams<kMultiMaxT>& P, const LaunchCtx& ctx, double2* partial,
-                               float* scale, double lr, double eta, double wd) {
+                               float* scale, unsigned int* count, double lr, double eta, double wd) {
     constexpr int G = Q8_GDT;
     constexpr int NS = G == G_F32 ? 3 : 4;
     constexpr int SUBT = G == G_F32 ? 256 : 128;
@@ -128,9 +151,13 @@ cudaError_t launch_layerwise_t(const StepParams<kMultiMaxT>& P, const LaunchCtx&
                 o = 1;
             return o;
         }();
+        // norms + per-tensor scales in one pass, then the step as a dependent launch (q8_layerwise.cuh)
         const int64_t g1 = std::min<int64_t>(P.total_blocks, static_cast<int64_t>(ctx.sms) * occ);
-        lars_norms_kernel<G, kMultiMaxT><<<static_cast<unsigned>(g1), kThreads, 0, ctx.stream>>>(P);
+        lars_norms_kernel<G, kMultiMaxT><<<static_cast<unsigned>(g1), kThreads, 0, ctx.stream>>>(P, count, scale);
         e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        return persistent_pdl(optim8bit_step_kernel<KIND, G, kMultiMaxT, SEARCH_BUCKET, NS, SUBT>, NS, SUBT,
+                              P.total_blocks, ctx, P, ctx.tabs);
     }
     if (e != cudaSuccess) return e;
     // partial slots written per block: the step kernel's warps per sub-block (LAMB) or 8 (LARS)
@@ -156,9 +183,10 @@ cudaError_t Q8_CAT(launch_step_g, Q8_GDT)(int kind, const StepParams<1>* single,
 
 namespace q8 {
 cudaError_t Q8_CAT(launch_layerwise_g, Q8_GDT)(int kind, const StepParams<kMultiMaxT>& P, const LaunchCtx& ctx,
-                                               double2* partial, float* scale, double lr, double eta, double wd) {
-    if (kind == KIND_LAMB) return launch_layerwise_t<KIND_LAMB>(P, ctx, partial, scale, lr, eta, wd);
-    if (kind == KIND_LARS) return launch_layerwise_t<KIND_LARS>(P, ctx, partial, scale, lr, eta, wd);
+                                               double2* partial, float* scale, unsigned int* count, double lr,
+                                               double eta, double wd) {
+    if (kind == KIND_LAMB) return launch_layerwise_t<KIND_LAMB>(P, ctx, partial, scale, count, lr, eta, wd);
+    if (kind == KIND_LARS) return launch_layerwise_t<KIND_LARS>(P, ctx, partial, scale, count, lr, eta, wd);
     return cudaErrorInvalidValue;
 }
 }  // namespace q8

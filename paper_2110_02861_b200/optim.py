@@ -355,7 +355,7 @@ class _LayerwiseOptimizer8bit(_Optimizer8bit):
                 tl = self._tensor_list(group, gdt, entries)
                 need = B.layerwise_workspace_bytes(tl)
                 if self._workspace is None or self._workspace.numel() < need:
-                    self._workspace = torch.empty(need, dtype=torch.uint8, device=tl.device)
+                    self._workspace = torch.zeros(need, dtype=torch.uint8, device=tl.device)  # zero-filled (q8.h)
                 scales = B.optim8bit_step_layerwise(self.kind, tl, lr=group["lr"], step=step, hp=hp,
                                                     trust_coefficient=eta, workspace=self._workspace).clone()
                 for i, e in enumerate(entries):

@@ -121,8 +121,9 @@ def test_layerwise_workspace_bytes():
     arr = (B.TensorDesc * 3)()
     for i, n in enumerate((5000, 0, 2048)):
         arr[i] = B.TensorDesc(FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, n)
-    # scales: 3 floats -> 16 B; partials: (3 + 0 + 1) blocks x 8 warp slots x 16 B; 16 B grid barrier
-    assert B.lib.q8_layerwise_workspace_bytes(arr, 3) == 16 + 4 * 128 + 16
+    # scales: 3 floats -> 16 B; partials: (3 + 0 + 1) blocks x 8 warp slots x 16 B; 384 LARS block
+    # counters; 16 B grid barrier
+    assert B.lib.q8_layerwise_workspace_bytes(arr, 3) == 16 + 4 * 128 + 4 * 384 + 16
     assert B.lib.q8_layerwise_workspace_bytes(arr, -1) == -1
 
 

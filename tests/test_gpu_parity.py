@@ -336,3 +336,40 @@ def test_linear_type_zero_round_trip(q8, signed):
     assert torch.all(d[::3] == 0.0) and torch.all(c_g.cpu()[::3] == (127 if signed else 0))
     a_t, c_t = q8.quantize_tensorwise(code_dev, x.to(DEV))
     assert torch.all(q8.dequantize_tensorwise(code_dev, c_t, a_t).cpu()[::3] == 0.0)
+
+
+# Ragged last blocks of multi-tensor launches ("n/B blocks" per tensor): tails of 5 .. 2032
+# elements, multiples of 16 and not, single-block tensors and tensors of several blocks, so one
+# sub-block's contiguous block range alternates tails (guarded direct loads) and full blocks (TMA stage);
+# two steps, every tensor bit for bit.
+TAIL_SIZES = [16, 2048 + 16, 48, 5, 2048 * 3 + 2032, 1024, 17, 2048 + 1008, 4096, 2048 + 1000, 64, 2048 * 2 + 32]
+
+
+@pytest.mark.parametrize("kind,gdt", [("momentum", "float16"), ("adam", "bfloat16"), ("adamw", "float32"),
+                                      ("momentum", "float32")])
+def test_multi_tensor_staged_tails(q8, kind, gdt):
+    hp = dict(synth.HPARAMS[kind])
+    two = kind != "momentum"
+    sizes = TAIL_SIZES * 6
+    ents, refs = [], []
+    for i, n in enumerate(sizes):
+        p = synth.params(n, seed=300 + i)
+        g = synth.grads(n, step=1, seed=300 + i, dtype=gdt)
+        s1, a1 = synth.random_state(n, seed=400 + i)
+        s2, a2 = synth.random_state(n, seed=500 + i, scale=1e-6)
+        ents.append((p.to(DEV), g.to(DEV), s1.to(DEV), s2.to(DEV) if two else None, a1.to(DEV),
+                     a2.to(DEV) if two else None))
+        refs.append([t.numpy().copy() for t in (p, s1, s2, a1, a2)] + [synth.to_f32_numpy(g)])
+    for t in (3, 4):
+        q8.optim8bit_step_multi(kind, ents, step=t, **hp)
+        for r in refs:
+            p, s1, s2, a1, a2, g = r
+            oracle.optim8bit_step(kind, p, g, s1, s2 if two else None, a1, a2 if two else None, step=t, **hp)
+    torch.cuda.synchronize()
+    for i, (e, r) in enumerate(zip(ents, refs)):
+        assert_same(e[0], r[0], f"t{i} p")
+        assert_same(e[2], r[1], f"t{i} s1")
+        assert_same(e[4], r[3], f"t{i} a1")
+        if two:
+            assert_same(e[3], r[2], f"t{i} s2")
+            assert_same(e[5], r[4], f"t{i} a2")
