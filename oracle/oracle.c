@@ -144,12 +144,33 @@ int oracle_linear_codebook(int is_signed, float out[256]) {
 /* ------------------------------------------------------------------------- */
 
 /*
+ * Exact difference a - b of two binary32 values as an unevaluated pair s + e of
+ * binary64 values: s = RN(a - b), e = the exact rounding error (Knuth's TwoSum
+ * of a and -b; every operation binary64 round-to-nearest, no contraction).
+ * A binary64 subtraction alone is NOT always exact here: for y = 1e-45 and
+ * Q = 1/255 the 2^141 exponent gap loses y entirely.
+ */
+static void exact_diff(float a, float b, double* s, double* e) {
+    double x = (double)a, c = -(double)b;
+    double sum = x + c;
+    double cv = sum - x;                 /* the part of c that made it into sum */
+    double xv = sum - cv;
+    *s = sum;
+    *e = (x - xv) + (c - cv);
+}
+
+/* Is the exact value s1 + e1 smaller than s2 + e2?  (s = RN(s + e), so the
+ * s parts order the exact values unless they are equal; then the errors do.) */
+static int pair_less(double s1, double e1, double s2, double e2) {
+    return s1 < s2 || (s1 == s2 && e1 < e2);
+}
+
+/*
  * Returns argmin_{j in 0..255} |Q[j] - y| with ties broken toward the lower
  * index (G6).  Q must be strictly ascending.  As Eq.3 says, the closest value
  * is found "via a binary search": lower_bound finds the first Q[hi] >= y, and
- * the answer is whichever of Q[hi-1], Q[hi] is closer.  The two distances are
- * compared in double, where the difference of two binary32 numbers that
- * bracket y is exact.
+ * the answer is whichever of Q[hi-1], Q[hi] is closer.  The two (non-negative)
+ * distances Q[hi] - y and y - Q[hi-1] are compared exactly (exact_diff).
  */
 int oracle_nearest_code(const float Q[256], float y) {
     int lo = 0, hi = 256;                        /* lower_bound over Q */
@@ -159,9 +180,10 @@ int oracle_nearest_code(const float Q[256], float y) {
     }
     if (hi == 0) return 0;
     if (hi == 256) return 255;
-    double d_lo = fabs((double)y - (double)Q[hi - 1]);
-    double d_hi = fabs((double)Q[hi] - (double)y);
-    return (d_hi < d_lo) ? hi : hi - 1;          /* tie -> lower index */
+    double s_lo, e_lo, s_hi, e_hi;
+    exact_diff(y, Q[hi - 1], &s_lo, &e_lo);
+    exact_diff(Q[hi], y, &s_hi, &e_hi);
+    return pair_less(s_hi, e_hi, s_lo, e_lo) ? hi : hi - 1;   /* tie -> lower index */
 }
 
 /* ------------------------------------------------------------------------- */

@@ -1,8 +1,12 @@
 """Pins for the oracle's nearest-code search (Eq.3; tie rule G6).
 
 The oracle uses a binary search plus a two-neighbour compare.  Here it is checked
-against brute force: np.argmin over all 256 exact float64 distances (np.argmin
-returns the FIRST minimum, i.e. ties go to the lower index)."""
+against brute force: np.argmin over all 256 float64 distances (np.argmin returns the
+FIRST minimum, i.e. ties go to the lower index) -- exact for the dynamic tables, whose
+midpoints are never far below the codes around them -- and, for any table, against
+an exact brute force over rational distances (fractions.Fraction)."""
+from fractions import Fraction
+
 import numpy as np
 import pytest
 
@@ -65,3 +69,43 @@ def test_random_matches_brute_force(signed):
         np.sign(rng.uniform(lo, 1.0, 20000)) * 10.0 ** rng.uniform(-9, 0, 20000),
     ]).astype(np.float32)
     assert np.array_equal(oracle.nearest_code(Q, y), brute(Q, y))
+
+
+def brute_exact(Q, y):
+    """argmin_j |Q_j - y| over exact rationals, first minimum (ties -> lower index, G6)."""
+    Qf = [Fraction(float(q)) for q in Q]
+    out = []
+    for v in np.asarray(y, np.float32):
+        yv = Fraction(float(v))
+        d = [abs(q - yv) for q in Qf]
+        out.append(d.index(min(d)))
+    return np.array(out, np.uint8)
+
+
+def _exact_tables():
+    sym = (np.arange(256, dtype=np.float64) * 2 / 255 - 1).astype(np.float32)   # no 0: a midpoint AT 0
+    wide = np.sort(np.concatenate([-np.logspace(-30, 0, 128), np.logspace(-30, 0, 128)])).astype(np.float32)
+    return {"dynamic_signed": oracle.dynamic_codebook(True), "symmetric_no_zero": sym, "wide_range": wide}
+
+
+@pytest.mark.parametrize("name", ["dynamic_signed", "symmetric_no_zero", "wide_range"])
+def test_matches_exact_rational_brute_force(name):
+    """Tiny inputs next to a midpoint at (or near) 0 are where a binary64 subtraction y - Q loses y (y = 1e-45,
+    Q = 1/255): the oracle must still return the exactly nearest code (Eq.3; G6)."""
+    Q = _exact_tables()[name]
+    rng = np.random.default_rng(5)
+    tiny = np.array([1e-45, 3e-45, 1e-40, 1e-38, 1e-30, 1e-20, 4.3e-19, 1e-10], np.float32)
+    mids = ((Q[:-1].astype(np.float64) + Q[1:]) / 2).astype(np.float32)
+    y = np.concatenate([tiny, -tiny, [0.0, -0.0, 1.0, -1.0], mids, np.nextafter(mids, np.float32(1)),
+                        np.nextafter(mids, np.float32(-1)), rng.uniform(-1, 1, 300),
+                        np.sign(rng.uniform(-1, 1, 300)) * 10.0 ** rng.uniform(-40, 0, 300)]).astype(np.float32)
+    assert np.array_equal(oracle.nearest_code(Q, y), brute_exact(Q, y))
+
+
+def test_exact_compare_fixes_lost_subtraction():
+    """The case that motivated the exact compare: y = 1e-45 is strictly closer to +1/255 than to -1/255,
+    but the binary64 distances both round to 1/255 (a false tie -> the lower index)."""
+    Q = _exact_tables()["symmetric_no_zero"]
+    assert int(oracle.nearest_code(Q, np.float32(1e-45))[0]) == 128
+    assert int(oracle.nearest_code(Q, np.float32(-1e-45))[0]) == 127
+    assert int(oracle.nearest_code(Q, np.float32(0.0))[0]) == 127       # exact tie -> lower
