@@ -28,7 +28,10 @@ namespace q8 {
 constexpr int kQNSub = 4, kQSubT = 256, kQStages = 3;
 constexpr uint32_t kQBarAddr = 0x7200;                   // [sub][stage] mbarriers
 constexpr uint32_t kQCntAddr = kQBarAddr + kQNSub * kQStages * 8;   // [sub][stage] release counters
-constexpr uint32_t kQGenRows = 0x20000;                  // GENERIC: 256 rows x 128 B (Eytzinger nodes)
+constexpr uint32_t kQGenSorted = 0x20000;                // GENERIC: 256 rows x 128 B, sorted T_c (T_255 = +inf)
+constexpr uint32_t kQGenRows = 0x28000;                  // GENERIC: 256 rows x 128 B (Eytzinger nodes)
+constexpr uint32_t kQGenT = kLutUAddr;                   // GENERIC: plain sorted T[256] for the table build (1 KB)
+constexpr int kQLutMinBlocksPerCta = 16;                 // GENERIC: build the bucket table only for launches this long
 constexpr int kQtSmemBytes = static_cast<int>(0x38000 - kDynBase);
 static_assert(kQCntAddr + kQNSub * kQStages * 4 <= 0x8000, "quantizer barriers below the free region");
 static_assert(kQNSub * kQStages <= 12, "stages: 8 in 0x10000-0x20000, 4 in 0x30000-0x38000");
@@ -94,9 +97,19 @@ __global__ void __launch_bounds__(kQNSub * kQSubT, 1)
             for (int i = tid; i < kLutUBytes / 16; i += nthr)
                 sts_u32x4(kLutUAddr + i * 16, lut[kLutSBytes / 16 + i]);
         }
-    } else {
-        // caller table: T_k = RD((Q_k + Q_{k+1})/2) (__fadd_rd rounds the exact sum down, halving is
-        // exact), node i of the Eytzinger tree = T_{rank(i)}, 32 lane copies per 128 B row
+    }
+    // caller table: T_k = RD((Q_k + Q_{k+1})/2) (__fadd_rd rounds the exact sum down, halving is
+    // exact), node i of the Eytzinger tree = T_{rank(i)}, 32 lane copies per 128 B row.  gen_fast: no
+    // threshold has 0 < |T| <= 2^-39 or T = 0, so the packed Markstein normalization (exactly RN(x/N)
+    // for |x/N| >= 2^-40) yields the same codes as the IEEE division: below 2^-39 both
+    // values lie on the same side of every threshold.
+    //   Long launches also build the step kernel's bucket table for the caller table (signed key layout,
+    //   q8_kernels.cuh "Bucketed search": LUT[key] = the code of the bucket's smallest value, from the
+    //   sorted thresholds) and check that no bucket spans more than two codes; if one does (a table
+    //   with codes closer than 1/64 of their binade), the launch keeps the 8-step descent.
+    bool gen_unsafe = false;
+    bool gen_lut = QTAB == QTAB_GENERIC && nblocks >= static_cast<int64_t>(kQLutMinBlocksPerCta) * gridDim.x;
+    if constexpr (QTAB == QTAB_GENERIC) {
         for (int i = tid; i < 256 * 8; i += nthr) {
             const int node = i >> 3, q = i & 7;
             float t = __int_as_float(0x7f800000);
@@ -104,15 +117,43 @@ __global__ void __launch_bounds__(kQNSub * kQSubT, 1)
                 const int level = 31 - __clz(node);
                 const int k = (2 * (node - (1 << level)) + 1) * (1 << (7 - level)) - 1;
                 t = __fmul_rn(__fadd_rd(code[k], code[k + 1]), 0.5f);
+                gen_unsafe |= fabsf(t) <= 0x1p-39f;
             }
             sts_f32x4(kQGenRows + node * 128 + q * 16, t);
+            const float ts = i < 255 * 8 ? __fmul_rn(__fadd_rd(code[i >> 3], code[(i >> 3) + 1]), 0.5f)
+                                         : __int_as_float(0x7f800000);
+            sts_f32x4(kQGenSorted + (i >> 3) * 128 + q * 16, ts);
+            if (q == 0) asm volatile("st.shared.f32 [%0], %1;" ::"r"(kQGenT + (i >> 3) * 4), "f"(ts) : "memory");
+        }
+        if (gen_lut) {
+            __syncthreads();
+            bool wide = false;
+            constexpr uint32_t kPos = 0x1FC1;  // keys of 0 <= y <= 1 (bits >> 17 <= 0x1FC0), likewise for y < 0
+            for (uint32_t i = tid; i < 2 * kPos; i += nthr) {
+                const uint32_t key = i < kPos ? i : 0x4000u + (i - kPos);
+                const bool neg = key >= 0x4000u;
+                const uint32_t mlo = (key << kShiftS) & 0x7fffffffu;
+                const uint32_t mhi = min(mlo + (1u << kShiftS) - 1u, 0x3f800000u);
+                const float a = __uint_as_float(mlo), bb = __uint_as_float(mhi);
+                const float lo = neg ? -bb : a, hi = neg ? -a : bb;  // the bucket's value range
+                uint32_t clo = 0, chi = 0;  // #{k : y > T_k}, branch-free binary search over T[0..255]
+#pragma unroll
+                for (uint32_t st = 128; st; st >>= 1) {
+                    clo += lo > lds_f32(kQGenT + (clo + st - 1) * 4) ? st : 0u;
+                    chi += hi > lds_f32(kQGenT + (chi + st - 1) * 4) ? st : 0u;
+                }
+                wide |= chi - clo > 1u;
+                asm volatile("st.shared.u8 [%0], %1;" ::"r"(kLutSAddr + key), "r"(clo) : "memory");
+            }
+            gen_lut = !__syncthreads_or(wide);
         }
     }
-    __syncthreads();
+    const bool gen_fast = !__syncthreads_or(gen_unsafe);
 
     const uint32_t red_base = kRedAddr + sub * (2 * 2 * kMaxSubWarps * 4);
     const uint32_t trow = kThreshAddr + lane4 + (kSigned ? 0u : 128u);
     const uint32_t grow = kQGenRows + lane4;
+    const uint32_t gsrow = kQGenSorted + lane4;
     const float Ntw = TW ? absmax[0] : 0.0f;
     uint32_t phase_bits = 0;  // bit s: parity of stage s
     int parity = 0;
@@ -214,20 +255,44 @@ __global__ void __launch_bounds__(kQNSub * kQSubT, 1)
             // flight per thread (the search is a chain of 8 dependent loads per element)
             float y[kSGroups * kVec];
             uint32_t i[kSGroups * kVec];
+            if (gen_fast && N >= 0x1p-70f && N < 0x1p126f) {  // block-uniform: packed Markstein division
+                const float rcp = __frcp_rn(N);
+                const f2 rc = pk(rcp, rcp), nN = pk(-N, -N);
 #pragma unroll
-            for (int c = 0; c < kSGroups; ++c)
+                for (int c = 0; c < kSGroups; ++c)
 #pragma unroll
-                for (int e = 0; e < kVec; ++e) {
-                    y[c * kVec + e] = N > 0.0f ? __fdiv_rn(v[c][e], N) : 0.0f;
-                    i[c * kVec + e] = 1u;
-                }
+                    for (int e = 0; e < kVec; e += 2) {
+                        const f2 xx = pk(v[c][e], v[c][e + 1]);
+                        const f2 q = fmul2(xx, rc);
+                        const f2 yy = ffma2(ffma2(q, nN, xx), rc, q);
+                        y[c * kVec + e] = lo_of(yy);
+                        y[c * kVec + e + 1] = hi_of(yy);
+                    }
+            } else {
 #pragma unroll
-            for (int l = 0; l < 8; ++l)
+                for (int c = 0; c < kSGroups; ++c)
 #pragma unroll
-                for (int j = 0; j < kSGroups * kVec; ++j) i[j] = 2u * i[j] + (y[j] > lds_f32(grow + (i[j] << 7)) ? 1u : 0u);
+                    for (int e = 0; e < kVec; ++e) y[c * kVec + e] = N > 0.0f ? __fdiv_rn(v[c][e], N) : 0.0f;
+            }
+            if (gen_lut) {  // bucket table + one compare against the sorted thresholds (128-B rows)
 #pragma unroll
-            for (int c = 0; c < kSGroups; ++c)
-                o[c] = pack4(i[c * kVec] - 256u, i[c * kVec + 1] - 256u, i[c * kVec + 2] - 256u, i[c * kVec + 3] - 256u);
+                for (int c = 0; c < kSGroups; ++c)
+                    o[c] = pack4(nearest_code<SEARCH_BUCKET, false, 7>(gsrow, y[c * kVec]),
+                                 nearest_code<SEARCH_BUCKET, false, 7>(gsrow, y[c * kVec + 1]),
+                                 nearest_code<SEARCH_BUCKET, false, 7>(gsrow, y[c * kVec + 2]),
+                                 nearest_code<SEARCH_BUCKET, false, 7>(gsrow, y[c * kVec + 3]));
+            } else {
+#pragma unroll
+                for (int j = 0; j < kSGroups * kVec; ++j) i[j] = 1u;
+#pragma unroll
+                for (int l = 0; l < 8; ++l)
+#pragma unroll
+                    for (int j = 0; j < kSGroups * kVec; ++j)
+                        i[j] = 2u * i[j] + (y[j] > lds_f32(grow + (i[j] << 7)) ? 1u : 0u);
+#pragma unroll
+                for (int c = 0; c < kSGroups; ++c)
+                    o[c] = pack4(i[c * kVec] - 256u, i[c * kVec + 1] - 256u, i[c * kVec + 2] - 256u, i[c * kVec + 3] - 256u);
+            }
         }
         // a7: store
 #pragma unroll

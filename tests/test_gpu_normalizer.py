@@ -41,11 +41,13 @@ def _blocks(N, bnd_f32):
     x = torch.zeros(nb, 2048, dtype=torch.float32, device=DEV)
     x[:, 0] = N
     base = bnd_f32[k][None, :] * N[:, None]                                 # RN(b_k * N)
+    # step by d ulps in the direction of increasing value, through the monotone integer key of the fp32
+    # order (key = bits for x >= +0, -(|bits| + 1) for x <= -0), so steps may cross zero (boundaries at
+    # the smallest denormals: a caller table whose midpoint is 0)
     bits = base.view(torch.int32)
-    # step |x| by d ulps in the direction of increasing value (negative values: bits move the other way)
-    step = torch.where(base < 0, -d[None, :], d[None, :])
-    stepped = (bits + step).view(torch.float32)
-    x[:, 1:2041] = torch.where(base == 0, base, stepped)
+    key = torch.where(bits >= 0, bits, -(bits & 0x7FFFFFFF) - 1) + d[None, :]
+    sign = torch.tensor(-0x80000000, dtype=torch.int32, device=DEV)
+    x[:, 1:2041] = torch.where(key >= 0, key, (-(key + 1)) | sign).view(torch.float32)
     x[:, 2041] = -N
     x[:, 2042] = N
     return x
@@ -56,8 +58,14 @@ def _expected(x, N, bnd64):
     return torch.searchsorted(bnd64, y.reshape(-1), right=True).reshape(x.shape)
 
 
-def _sweep(q8, signed, N, chunk=1 << 17):
-    Q = oracle.dynamic_codebook(signed)
+def _sweep(q8, signed, N, chunk=1 << 17, Q=None):
+    """Q None: the built-in dynamic table (q8_quantize_blockwise_dynamic); else the caller table Q through
+    q8_quantize_blockwise (its own thresholds; the packed Markstein normalization when no threshold lies
+    within 2^-39 of 0, else the IEEE division)."""
+    generic = Q is not None
+    if Q is None:
+        Q = oracle.dynamic_codebook(signed)
+    code_dev = torch.from_numpy(np.ascontiguousarray(Q, np.float32)).to(DEV)
     bnd = _boundaries(Q)
     bnd64 = torch.from_numpy(bnd).to(DEV)
     bnd32 = torch.from_numpy(bnd.astype(np.float32)).to(DEV)
@@ -67,7 +75,10 @@ def _sweep(q8, signed, N, chunk=1 << 17):
         x = _blocks(Nc, bnd32)
         if not signed:
             x = x.abs()    # unsigned table: non-negative states; boundaries are all >= 0
-        a, c = q8.quantize_blockwise_dynamic(signed, x.reshape(-1))
+        if generic:
+            a, c = q8.quantize_blockwise(code_dev, x.reshape(-1))
+        else:
+            a, c = q8.quantize_blockwise_dynamic(signed, x.reshape(-1))
         assert torch.equal(a.view(torch.int32), Nc.abs().view(torch.int32)), "absmax != N"
         exp = _expected(x, Nc, bnd64)
         bad += int((c.view(x.shape).to(torch.int64) != exp).sum())
@@ -116,3 +127,42 @@ def test_normalizer_blocks_vs_oracle_codec(q8, signed):
     a_r, c_r = oracle.quantize_blockwise(Q, x.cpu().numpy())
     assert_same(a, a_r, "absmax")
     assert_same(c, c_r, "codes")
+
+
+def _caller_tables():
+    rng = np.random.default_rng(3)
+    quant = oracle.quantile_codebook(oracle.exact_quantiles(rng.standard_normal(1 << 16).astype(np.float32)))
+    tiny = oracle.dynamic_codebook(True).copy()
+    assert tiny[127] == 0.0
+    tiny[128], tiny[129] = np.float32(1e-13), np.float32(2e-13)
+    return {
+        "dynamic_signed": (True, oracle.dynamic_codebook(True)),
+        "dynamic_unsigned": (False, oracle.dynamic_codebook(False)),
+        "linear_signed": (True, oracle.linear_codebook(True)),      # exact 0 code: thresholds +-1/256
+        "quantile": (True, quant),                                   # Eq.5 quantile data type
+        # symmetric grid without 0: a threshold at exactly 0 -> the kernel keeps the IEEE division
+        "symmetric_no_zero": (True, (np.arange(256, dtype=np.float64) * 2 / 255 - 1).astype(np.float32)),
+        # codes 1e-13, 2e-13 next to 0: thresholds below 2^-39 -> the IEEE division
+        "tiny_codes": (True, tiny),
+        # 128 codes packed into [0.87, 1]: buckets of the top binade span up to ~9 codes -> the long launch
+        # rejects the bucket table and keeps the 8-step descent
+        "dense_top": (True, np.concatenate([np.linspace(-1, 0.86, 128), np.linspace(0.87, 1, 128)]).astype(np.float32)),
+    }
+
+
+@pytest.mark.parametrize("name", ["dynamic_signed", "dynamic_unsigned", "linear_signed", "quantile",
+                                  "symmetric_no_zero", "tiny_codes", "dense_top"])
+def test_normalizer_binades_caller_table(q8, name):
+    """The generic (caller-table) quantizer on the adversarial blocks: sampled mantissas (2^12 per binade)
+    across and outside the fast range, every decision boundary of the table at -4..+3 ulps.  The launches
+    are long enough (>= 16 blocks per CTA) for the per-CTA bucket table (q8_quant_kernel.cuh), so this
+    covers it, its rejection (dense_top) and both normalizations."""
+    signed, Q = _caller_tables()[name]
+    g = torch.Generator(device=DEV)
+    g.manual_seed(321)
+    Ns = []
+    for e in (-80, -70, -69, -40, -1, 0, 1, 60, 125, 126):
+        m = torch.randint(0, 1 << 23, (1 << 12,), generator=g, device=DEV, dtype=torch.int32)
+        m[:2] = torch.tensor([0, (1 << 23) - 1], device=DEV, dtype=torch.int32)
+        Ns.append(((e + 127) << 23 | m).view(torch.float32))
+    assert _sweep(q8, signed, torch.cat(Ns), Q=Q) == 0
