@@ -196,3 +196,28 @@ def test_lars_one_launch_variant():
                        timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+def test_lars_workspace_counters_return_to_zero(q8):
+    """The LARS norms pass counts every tensor's blocks in the workspace (q8.h: the workspace must be zero-filled
+    before its first use and every call leaves it so): after each of several calls -- chunked launches, empty
+    tensors, tensors of one and of many blocks -- the counter region is zero again."""
+    sizes = [0, 5, 2048, 4096 + 17, 70_000, 0, 3] * 60   # 420 tensors: two launch chunks
+    ents, _ = _make("lars", sizes, "float16", seed0=50)
+    for i, (e, n) in enumerate(zip(ents, sizes)):
+        e[1] = synth.grads(n, step=1, seed=9 + i, dtype="float16").to(DEV)
+    tl = q8.TensorList([tuple(e) for e in ents], "lars")
+    need = q8.layerwise_workspace_bytes(tl)
+    ws = torch.zeros(need, dtype=torch.uint8, device=DEV)
+    first = None
+    for t in (1, 2, 3):
+        scales = q8.optim8bit_step_layerwise("lars", tl, step=t, trust_coefficient=ETA, workspace=ws, **LARS).clone()
+        torch.cuda.synchronize()
+        counters = ws[need - 16 - 4 * 384:need - 16]
+        assert int(counters.count_nonzero()) == 0, f"call {t}: block counters not reset"
+        if first is None:
+            first = scales
+    # every tensor got a finite scale; empty ones lr (q8.h)
+    sc = first.cpu().numpy()
+    assert np.all(np.isfinite(sc))
+    assert np.all(sc[[i for i, n in enumerate(sizes) if n == 0]] == np.float32(LARS["lr"]))
