@@ -222,22 +222,25 @@ q8_status q8_optim32bit_step_multi(q8_kind kind, q8_dtype g_dtype, const q8_tens
  * the scales (the CTA that finishes a tensor's last block sums its partials), then the fused step as a
  * programmatic dependent launch (it stages its tables while the norms pass drains).
  *   workspace_dev  device scratch of at least q8_layerwise_workspace_bytes(tensors, n) bytes,
- *                  16-B aligned, caller-owned, ZERO-FILLED before its first use (it holds block
- *                  counters that every call leaves at zero again); must not be used by another call
- *                  until this one completes on `stream`.  On completion its first 4*num_tensors bytes hold each
+ *                  16-B aligned, caller-owned; its first Q8_LAYERWISE_SCALE_OFFSET bytes (block
+ *                  counters of the LARS norms pass, at a fixed offset for any tensor list) must be
+ *                  ZERO before the first call that uses it, and every call leaves them zero again;
+ *                  must not be used by another call until this one completes on `stream`.  On
+ *                  completion the 4*num_tensors bytes at offset Q8_LAYERWISE_SCALE_OFFSET hold each
  *                  tensor's fp32 scale (float scale[i] for tensors_host[i]; lr for empty tensors)
  *                  -- the trust ratio times lr, a diagnostic output.
  * Other arguments, alignment and errors as q8_optim8bit_step_multi; INVALID also for a kind
  * other than LAMB/LARS, trust_coefficient <= 0 (LARS) or a too-small workspace. */
+#define Q8_LAYERWISE_SCALE_OFFSET 1552  /* bytes: 4 * Q8_MAX_TENSORS_PER_LAUNCH counters + 16 */
 q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_tensor* tensors_host,
                                       int32_t num_tensors, int32_t blocksize, const q8_hparams* hp,
                                       double trust_coefficient, int64_t step, void* workspace_dev,
                                       int64_t workspace_bytes, void* stream);
 
-/* Bytes of workspace q8_optim8bit_step_layerwise needs for these tensors (host function): 4 per
- * tensor (rounded up to 16) + 128 per 2048-block of the largest launch chunk (binary64 partial
- * norms per warp) + 4 * Q8_MAX_TENSORS_PER_LAUNCH (per-tensor block counters of the LARS norms pass)
- * + 16 (the grid barrier of the one-launch LARS step).  -1 on bad input. */
+/* Bytes of workspace q8_optim8bit_step_layerwise needs for these tensors (host function):
+ * 4 * Q8_MAX_TENSORS_PER_LAUNCH (per-tensor block counters of the LARS norms pass) + 16 (the grid
+ * barrier of the one-launch LARS step) + 4 per tensor (the scales, rounded up to 16) + 128 per
+ * 2048-block of the largest launch chunk (binary64 partial norms per warp).  -1 on bad input. */
 int64_t q8_layerwise_workspace_bytes(const q8_tensor* tensors_host, int32_t num_tensors);
 
 /* Fused ZeRO-1 step over peer memory: ONE kernel per rank does

@@ -17,6 +17,7 @@ Q8_F32, Q8_F16, Q8_BF16 = 0, 1, 2
 Q8_ADAM, Q8_ADAMW, Q8_MOMENTUM, Q8_LAMB, Q8_LARS = 0, 1, 2, 3, 4
 MAX_TENSORS_PER_LAUNCH = 384
 BLOCKSIZE = 2048
+Q8_LAYERWISE_SCALE_OFFSET = 1552  # include/q8.h: the layer-wise scales' byte offset in the workspace
 
 KINDS = {"adam": Q8_ADAM, "adamw": Q8_ADAMW, "momentum": Q8_MOMENTUM, "lamb": Q8_LAMB, "lars": Q8_LARS}
 GDTYPES = {torch.float32: Q8_F32, torch.float16: Q8_F16, torch.bfloat16: Q8_BF16}
@@ -394,7 +395,7 @@ def optim8bit_step_layerwise(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1
                                                float(trust_coefficient), int(step),
                                                _dev_ptr(workspace, torch.uint8, "workspace", tl.device),
                                                workspace.numel(), _stream(tl.device)))
-    return workspace[:4 * tl.count].view(torch.float32)
+    return workspace[Q8_LAYERWISE_SCALE_OFFSET:Q8_LAYERWISE_SCALE_OFFSET + 4 * tl.count].view(torch.float32)
 
 
 def zero_signal_bytes(world: int, num_ctas: int = 0) -> int:

@@ -614,7 +614,12 @@ constexpr int kLwChunk = Q8_MAX_TENSORS_PER_LAUNCH;
 
 // Workspace layout: float scale[num_tensors] (rounded up to 16 B), then double2 partial[] sized
 // for the largest chunk of kLwChunk consecutive tensors.
-constexpr int64_t kLwCountBytes = 4 * kLwChunk;  // zero between calls (the norms pass resets them)
+// Workspace layout (q8.h): [0, kLwCountBytes) the per-tensor block counters of the LARS norms pass (zero
+// between calls: the pass resets them) -- at a FIXED offset, so a workspace reused for other tensor lists
+// still finds them zero; then the 16-B grid barrier of the one-launch LARS step; then the scales
+// (Q8_LAYERWISE_SCALE_OFFSET); then the binary64 partials.
+constexpr int64_t kLwCountBytes = 4 * kLwChunk;
+static_assert(kLwCountBytes + 16 == Q8_LAYERWISE_SCALE_OFFSET, "q8.h scale offset");
 int64_t lw_scale_bytes(int32_t num_tensors) { return (static_cast<int64_t>(num_tensors) * 4 + 15) / 16 * 16; }
 
 int64_t lw_partial_blocks(const q8_tensor* t, int32_t num_tensors) {
@@ -663,15 +668,16 @@ q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_t
                     static_cast<long long>(need));
     DeviceState* d = nullptr;
     if (q8_status s = device_state(&d); s != Q8_OK) return s;
-    float* scale = static_cast<float*>(workspace_dev);
-    double2* partial = reinterpret_cast<double2*>(static_cast<uint8_t*>(workspace_dev) + lw_scale_bytes(num_tensors));
+    uint8_t* const ws = static_cast<uint8_t*>(workspace_dev);
+    unsigned int* count = reinterpret_cast<unsigned int*>(ws);
+    float* scale = reinterpret_cast<float*>(ws + Q8_LAYERWISE_SCALE_OFFSET);
+    double2* partial = reinterpret_cast<double2*>(ws + Q8_LAYERWISE_SCALE_OFFSET + lw_scale_bytes(num_tensors));
     static thread_local q8::StepParams<kLwChunk> P;
     P.s = make_scalars(hp, step, kind);
     P.lw.lr = hp->lr;
     P.lw.eta = trust_coefficient;
     P.lw.wd = hp->weight_decay;
-    P.lw.gbar = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(workspace_dev) + need - 16);
-    unsigned int* count = reinterpret_cast<unsigned int*>(static_cast<uint8_t*>(workspace_dev) + need - 16 - kLwCountBytes);
+    P.lw.gbar = reinterpret_cast<unsigned int*>(ws + kLwCountBytes);
     const q8::LaunchCtx ctx{d->tabs, d->sms, static_cast<cudaStream_t>(stream), q8::SEARCH_BUCKET, 0, 0};
     for (int32_t c = 0; c < num_tensors; c += kLwChunk) {
         // every tensor of the chunk keeps its slot (empty ones have no blocks) so that

@@ -117,6 +117,13 @@ def _lw(kind=B.Q8_LAMB, trust=0.001, ws=FAKE, ws_bytes=1 << 20, arr=None, count=
                                              trust, 1, ws, ws_bytes, None)
 
 
+def test_layerwise_scale_offset_matches_header():
+    import re
+    hdr = open(os.path.join(os.path.dirname(__file__), "..", "include", "q8.h")).read()
+    m = re.search(r"#define Q8_LAYERWISE_SCALE_OFFSET (\d+)", hdr)
+    assert m and int(m.group(1)) == B.Q8_LAYERWISE_SCALE_OFFSET == 4 * 384 + 16
+
+
 def test_layerwise_workspace_bytes():
     arr = (B.TensorDesc * 3)()
     for i, n in enumerate((5000, 0, 2048)):

@@ -213,7 +213,7 @@ def test_lars_workspace_counters_return_to_zero(q8):
     for t in (1, 2, 3):
         scales = q8.optim8bit_step_layerwise("lars", tl, step=t, trust_coefficient=ETA, workspace=ws, **LARS).clone()
         torch.cuda.synchronize()
-        counters = ws[need - 16 - 4 * 384:need - 16]
+        counters = ws[:4 * 384]
         assert int(counters.count_nonzero()) == 0, f"call {t}: block counters not reset"
         if first is None:
             first = scales
@@ -221,3 +221,32 @@ def test_lars_workspace_counters_return_to_zero(q8):
     sc = first.cpu().numpy()
     assert np.all(np.isfinite(sc))
     assert np.all(sc[[i for i, n in enumerate(sizes) if n == 0]] == np.float32(LARS["lr"]))
+
+
+def test_lars_workspace_reused_across_tensor_lists(q8):
+    """One workspace serves a long list and then a short one (an optimizer with several parameter groups):
+    the counters sit at a fixed offset (q8.h), so the short list's step is bit-exact against the oracle
+    (teacher-forced with the GPU's scales, each within one fp32 ulp of the oracle's own, reading L3)."""
+    sizes_a = [70_000, 5, 2048, 300_000, 17] * 20
+    sizes_b = [4096 + 1, 9, 50_000]
+    ea, _ = _make("lars", sizes_a, "bfloat16", seed0=300)
+    eb, rb = _make("lars", sizes_b, "bfloat16", seed0=400)
+    for i, (e, n) in enumerate(zip(ea, sizes_a)):
+        e[1] = synth.grads(n, step=1, seed=5 + i, dtype="bfloat16").to(DEV)
+    ws = torch.zeros(q8.layerwise_workspace_bytes([tuple(e) for e in ea]), dtype=torch.uint8, device=DEV)
+    q8.optim8bit_step_layerwise("lars", [tuple(e) for e in ea], step=1, trust_coefficient=ETA, workspace=ws, **LARS)
+    gs = [synth.grads(n, step=2, seed=50 + i, dtype="bfloat16") for i, n in enumerate(sizes_b)]
+    for e, g in zip(eb, gs):
+        e[1] = g.to(DEV)
+    got = q8.optim8bit_step_layerwise("lars", [tuple(e) for e in eb], step=2, trust_coefficient=ETA, workspace=ws,
+                                      **LARS).cpu().numpy()
+    torch.cuda.synchronize()
+    for i, (r, g) in enumerate(zip(rb, gs)):
+        gf = synth.to_f32_numpy(g)
+        c = [x.copy() for x in r]
+        exp = oracle.optim8bit_layerwise_step("lars", c[0], gf, c[1], None, c[3], None, step=2,
+                                              trust_coefficient=ETA, **LARS)
+        assert abs(float(got[i]) - float(exp)) <= float(np.spacing(np.float32(exp))), f"scale {i}"
+        oracle.optim8bit_layerwise_step("lars", r[0], gf, r[1], None, r[3], None, step=2, trust_coefficient=ETA,
+                                        forced_scale=float(got[i]), **LARS)
+    _assert_equal("lars", eb, rb)
