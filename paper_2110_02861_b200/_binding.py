@@ -377,8 +377,11 @@ def optim8bit_step_layerwise(kind, tensors, *, lr, beta1=0.9, beta2=0.999, eps=1
                              bias_correction=True, step=1, trust_coefficient=0.001, blocksize=BLOCKSIZE,
                              workspace: torch.Tensor | None = None, hp: HParams | None = None) -> torch.Tensor:
     """One 8-bit LAMB / LARS step over many tensors (each tensor is one layer: its own trust
-    ratio).  entries as optim8bit_step_multi (s2/absmax2 None for LARS).  Returns the float32
-    per-tensor scales RN(lr * ratio) (a view into the workspace, valid until its next use)."""
+    ratio).  entries as optim8bit_step_multi (s2/absmax2 None for LARS).  workspace: a uint8 device
+    tensor of at least layerwise_workspace_bytes() bytes whose first Q8_LAYERWISE_SCALE_OFFSET bytes
+    are zero before its first use (torch.zeros; every call leaves them zero); None or too small:
+    a zero-filled one is allocated.  Returns the float32 per-tensor scales RN(lr * ratio) (a view
+    into the workspace, valid until its next use)."""
     kind = KINDS.get(kind, kind)
     tl = tensors if isinstance(tensors, TensorList) else TensorList(tensors, kind)
     if tl.count == 0:
