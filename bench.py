@@ -877,6 +877,16 @@ def main_layerwise(args, cfg, q8, world, rank, local, dev):
         dist.destroy_process_group()
 
 
+def committed_traffic(workload, world):
+    """DRAM bytes per launch of the workload's dominant kernel from its committed ncu capture
+    (profiles/traffic_<workload>.json), single-GPU lines only; None if there is none."""
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
+    if world == 1 and os.path.exists(tpath):
+        with open(tpath) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    return None
+
+
 def main_multi(args, cfg, q8, world, rank, local, dev):
     """Multi-tensor workloads (BASELINE config 3: 8-bit Momentum over ResNet-50's 161 tensors, 99 of
     them smaller than one block): per-tensor blocks, the tensors are views of one flat
@@ -990,7 +1000,8 @@ def main_multi(args, cfg, q8, world, rank, local, dev):
             "data": f"synthetic: p~N(0,0.02^2), {gdt} g~N(0,1e-3^2) (pool of 2), states evolved from zero",
             "config": cfg,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "bytes_per_param": bpp, "algorithmic_bytes_per_launch": n_total * bpp,
+                         "traffic": committed_traffic(args.workload, world), "bytes_per_param": bpp,
+                         "algorithmic_bytes_per_launch": n_total * bpp,
                          "kernel": "optim8bit_step_kernel (multi-tensor plan, one launch)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
                          else "fallback 6.65 TB/s (B200_PROFILING.md)"},
