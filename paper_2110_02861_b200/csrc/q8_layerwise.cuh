@@ -5,7 +5,9 @@
 // A layer-wise step needs per-tensor norms before any parameter can move, so it is three
 // stream-ordered launches per chunk of <= 384 tensors (LARS: two -- its norms pass also computes the
 // scales, lars_norms_kernel below):
-//   1. norms pass           per 2048-block partial sums (binary64) of w^2 and of x^2, where
+//   1. norms pass           partial sums (binary64) of w^2 and of x^2 -- LAMB: one per warp per
+//                           run of consecutive blocks of one tensor (segment) that a sub-block steps,
+//                           in the slot of the segment's last block (+0 in the others) --, where
 //                           x = u (LAMB: the update direction from the fp32 post-update states,
 //                           computed exactly as pass 3 computes it -- the fused step kernel in
 //                           MODE_NORMS: same TMA stages, decode and update, no stores) or x = g
