@@ -7,12 +7,12 @@
 // scales, lars_norms_kernel below):
 //   1. norms pass           partial sums (binary64) of w^2 and of x^2 -- LAMB: one per warp per
 //                           run of consecutive blocks of one tensor (segment) that a sub-block steps,
-//                           in the slot of the segment's last block (+0 in the others) --, where
+//                           in the slot of the segment's last block --, where
 //                           x = u (LAMB: the update direction from the fp32 post-update states,
 //                           computed exactly as pass 3 computes it -- the fused step kernel in
 //                           MODE_NORMS: same TMA stages, decode and update, no stores) or x = g
 //                           (LARS: lars_norms_kernel); no writes besides the partials (16 B/block)
-//   2. layer_scale_kernel   one CTA per tensor: sums its partials in a fixed order, then the
+//   2. lamb_scale_kernel    one CTA per tensor: sums its partials in a fixed order, then the
 //                           tensor's scale a = RN(lr * ratio) (binary64 ratio, L3)
 //   3. optim8bit_step_kernel<KIND_LAMB / KIND_LARS>  the fused step with the tensor's scale
 // HBM traffic per parameter with bf16 grads: LAMB 8 B (pass 1) + 14 B (pass 3); LARS 6 B + 12 B.
@@ -151,12 +151,72 @@ __global__ void __launch_bounds__(kThreads) lars_norms_kernel(const __grid_const
     lars_count_tensor<MAXT>(P, ti, seg, count, scale, red[0], &last);
 }
 
+// LAMB: one CTA per tensor of the launch, ||w|| and ||u|| from the norms pass's segment partials.  The
+// pass (MODE_NORMS of the step kernel) gives sub-block q of its Q = nsubs sub-blocks the block range
+// [q*B/Q, (q+1)*B/Q) and writes, per warp, one partial pair per run of that range inside one tensor,
+// in the slot of the run's last block.  Tensor t's blocks [bs, be) meet the ranges q0..q1 (those
+// holding bs and be-1); the run of range q ends at min(be, (q+1)*B/Q) - 1.  Fixed summation order:
+// thread-strided over q, slots in order, warp butterfly, warps in order (L3); then as below,
+//   a = RN(lr * (||w|| / ||u||))   (lr when either norm is 0)
+__device__ __forceinline__ int64_t range_start(int64_t q, int64_t B, int64_t Q) { return q * B / Q; }
+__device__ __forceinline__ int64_t range_of_block(int64_t x, int64_t B, int64_t Q) {
+    int64_t q = x * Q / B;  // within one of the answer; settle it with the kernel's own arithmetic
+    while (q + 1 < Q && range_start(q + 1, B, Q) <= x) ++q;
+    while (q > 0 && range_start(q, B, Q) > x) --q;
+    return q;
+}
+constexpr int kScaleThreads = 1024;
+template <int MAXT>
+__global__ void __launch_bounds__(kScaleThreads) lamb_scale_kernel(const __grid_constant__ StepParams<MAXT> P,
+                                                                   const double2* __restrict__ partial,
+                                                                   float* __restrict__ scale, double lr, int wpb,
+                                                                   int64_t nsubs) {
+    __shared__ double red[2][kScaleThreads / 32];
+    const int t = blockIdx.x, tid = threadIdx.x;
+    const int64_t bs = P.block_start[t], be = P.block_start[t + 1], B = P.total_blocks, Q = nsubs;
+    double sw = 0.0, sx = 0.0;
+    if (be > bs) {
+        const int64_t q0 = range_of_block(bs, B, Q), q1 = range_of_block(be - 1, B, Q);
+        for (int64_t q = q0 + tid; q <= q1; q += kScaleThreads) {
+            const int64_t r0 = range_start(q, B, Q), r1 = range_start(q + 1, B, Q);
+            if (r0 == r1) continue;  // an empty range (fewer blocks than sub-blocks)
+            const int64_t end = (be < r1 ? be : r1) - 1;
+            double2 v[kNormSlots];
+#pragma unroll
+            for (int k = 0; k < kNormSlots; ++k)
+                if (k < wpb) v[k] = partial[end * kNormSlots + k];
+#pragma unroll
+            for (int k = 0; k < kNormSlots; ++k)
+                if (k < wpb) {
+                    sw += v[k].x;
+                    sx += v[k].y;
+                }
+        }
+    }
+    sw = warp_sum_f64(sw);
+    sx = warp_sum_f64(sx);
+    if ((tid & 31) == 0) {
+        red[0][tid >> 5] = sw;
+        red[1][tid >> 5] = sx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        sw = sx = 0.0;
+        for (int k = 0; k < kScaleThreads / 32; ++k) {
+            sw += red[0][k];
+            sx += red[1][k];
+        }
+        const double wn = sqrt(sw), xn = sqrt(sx);
+        scale[t] = static_cast<float>(lr * (wn > 0.0 && xn > 0.0 ? wn / xn : 1.0));
+    }
+}
+
 // One CTA (kThreads) per tensor of the launch: ||w|| and ||x|| from its per-warp block partials
 // (wpb of the kNormSlots slots per block; fixed summation order: thread-strided over blocks, slots in
 // order, warp butterfly, warps in order), then the fp32 scale (L1-L3):
 //   LAMB  a = RN(lr * (||w|| / ||u||))                    (1 when either norm is 0)
 //   LARS  a = RN(lr * (eta ||w|| / (||g|| + wd ||w||)))   (lr when either norm is 0)
-constexpr int kScaleThreads = 1024;
+// (LAMB now uses lamb_scale_kernel above; this per-block form serves the lists with no blocks at all)
 template <int KIND, int MAXT>
 __global__ void __launch_bounds__(kScaleThreads) layer_scale_kernel(const __grid_constant__ StepParams<MAXT> P,
                                                                     const double2* __restrict__ partial,

@@ -14,13 +14,18 @@
 namespace q8 {
 namespace {
 
+// Grid of a persistent step launch: one CTA per SM, fewer when there are fewer blocks than sub-blocks.
+int64_t persistent_grid(int64_t work_blocks, int nsub, int sms) {
+    const int64_t grid = (work_blocks + nsub - 1) / nsub;
+    return grid > sms ? sms : grid;
+}
+
 template <typename Kern, typename... Args>
 cudaError_t persistent(Kern fn, int nsub, int subt, int64_t work_blocks, const LaunchCtx& ctx, const Args&... args) {
     const int smem = step_smem_bytes(nsub, Q8_GDT);
     cudaError_t e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
     if (e != cudaSuccess) return e;
-    int64_t grid = (work_blocks + nsub - 1) / nsub;
-    if (grid > ctx.sms) grid = ctx.sms;
+    const int64_t grid = persistent_grid(work_blocks, nsub, ctx.sms);
     fn<<<static_cast<unsigned>(grid), nsub * subt, smem, ctx.stream>>>(args...);
     return cudaGetLastError();
 }
@@ -160,10 +165,11 @@ cudaError_t launch_layerwise_t(const StepParams<kMultiMaxT>& P, const LaunchCtx&
                               P.total_blocks, ctx, P, ctx.tabs);
     }
     if (e != cudaSuccess) return e;
-    // partial slots written per block: the step kernel's warps per sub-block (LAMB) or 8 (LARS)
-    const int wpb = KIND == KIND_LAMB ? SUBT / 32 : kWarps;
-    layer_scale_kernel<KIND, kMultiMaxT><<<P.num_tensors, kScaleThreads, 0, ctx.stream>>>(P, partial, scale, lr, eta, wd,
-                                                                                    wpb);
+    // LAMB (the only kind that gets here): the norms pass wrote one partial per warp per tensor segment of
+    // each of its grid * NS sub-blocks, in the slot of the segment's last block
+    const int64_t nsubs = persistent_grid(P.total_blocks, NS, ctx.sms) * NS;
+    lamb_scale_kernel<kMultiMaxT><<<P.num_tensors, kScaleThreads, 0, ctx.stream>>>(P, partial, scale, lr, SUBT / 32,
+                                                                                  nsubs);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     return persistent(optim8bit_step_kernel<KIND, G, kMultiMaxT, SEARCH_BUCKET, NS, SUBT>, NS, SUBT, P.total_blocks,

@@ -113,14 +113,31 @@ def test_layerwise_zero_tensors_and_empty(q8, kind):
     _assert_equal(kind, ents, refs)
 
 
-def test_layerwise_chunks_over_384_tensors(q8):
+@pytest.mark.parametrize("gdt", ["float32", "bfloat16"])
+def test_lamb_norm_segments_span_blocks_and_tensors(q8, gdt):
+    """LAMB's norms pass keeps running sums over a sub-block's consecutive blocks of one tensor and
+    reduces once per segment (DESIGN 6.10): ~3,400 blocks give every sub-block several blocks, with
+    ranges that start and end inside tensors and cross short tensors.  Scales within 1 fp32 ulp (L3),
+    then teacher-forced: every output bit for bit."""
+    sizes = [3_000_000, 5, 2_500_007, 2049, 1, 1_500_000, 4095]
+    ents, refs = _make("lamb", sizes, gdt, seed0=77)
+    for t in (1, 2):
+        got, exp = _step_both(q8, "lamb", ents, refs, sizes, gdt, t, HP["lamb"], teacher_force=True)
+        ulps = np.abs(got.view(np.int32).astype(np.int64) - exp.view(np.int32).astype(np.int64))
+        assert ulps.max() <= 1, (got, exp)
+        _assert_equal("lamb", ents, refs)
+
+
+@pytest.mark.parametrize("kind", ["lars", "lamb"])
+def test_layerwise_chunks_over_384_tensors(q8, kind):
     """More tensors than one launch takes: the workspace's partials are reused per chunk."""
     rng = np.random.default_rng(5)
     sizes = [int(x) for x in rng.integers(1, 9000, size=400)]
-    ents, refs = _make("lars", sizes, "bfloat16")
-    got, exp = _step_both(q8, "lars", ents, refs, sizes, "bfloat16", 1, LARS)
-    assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
-    _assert_equal("lars", ents, refs)
+    ents, refs = _make(kind, sizes, "bfloat16")
+    got, exp = _step_both(q8, kind, ents, refs, sizes, "bfloat16", 1, HP[kind], teacher_force=True)
+    ulps = np.abs(got.view(np.int32).astype(np.int64) - exp.view(np.int32).astype(np.int64))
+    assert ulps.max() <= 1, (got, exp)
+    _assert_equal(kind, ents, refs)
 
 
 def test_lars_resnet50_layer_list(q8):
