@@ -632,6 +632,50 @@ int64_t lw_partial_blocks(const q8_tensor* t, int32_t num_tensors) {
     return best;
 }
 
+// The layer-wise launches, chunk by chunk of <= MAXT tensors, with descriptor table P (MAXT = kLwChunk, or
+// kSmallMaxT for short lists).
+template <int MAXT>
+q8_status layerwise_chunks(q8::StepParams<MAXT>& P, q8_kind kind, q8_dtype g_dtype, const q8_tensor* tensors_host,
+                           int32_t num_tensors, const q8_hparams* hp, double trust_coefficient, int64_t step,
+                           uint8_t* ws, const q8::LaunchCtx& ctx) {
+    unsigned int* count = reinterpret_cast<unsigned int*>(ws);
+    float* scale = reinterpret_cast<float*>(ws + Q8_LAYERWISE_SCALE_OFFSET);
+    double2* partial = reinterpret_cast<double2*>(ws + Q8_LAYERWISE_SCALE_OFFSET + lw_scale_bytes(num_tensors));
+    P.s = make_scalars(hp, step, kind);
+    P.lw.lr = hp->lr;
+    P.lw.eta = trust_coefficient;
+    P.lw.wd = hp->weight_decay;
+    P.lw.gbar = reinterpret_cast<unsigned int*>(ws + kLwCountBytes);
+    for (int32_t c = 0; c < num_tensors; c += MAXT) {
+        // every tensor of the chunk keeps its slot (empty ones have no blocks) so that
+        // scale[i] belongs to tensors_host[i]
+        const int k = std::min(num_tensors - c, MAXT);
+        int64_t blocks = 0;
+        for (int j = 0; j < k; ++j) {
+            const q8_tensor& t = tensors_host[c + j];
+            P.t[j] = q8::TensorDesc{t.p, t.g, t.s1, t.s2, t.absmax1, t.absmax2, t.n};
+            P.block_start[j] = blocks;
+            blocks += (t.n + q8::kBlock - 1) / q8::kBlock;
+        }
+        P.num_tensors = k;
+        P.block_start[k] = blocks;
+        P.total_blocks = blocks;
+        P.scale = scale + c;
+        P.partial = partial;
+        cudaError_t e = cudaErrorInvalidValue;
+        switch (g_dtype) {
+            case Q8_F32: e = q8::launch_layerwise_g0(kind, P, ctx, partial, scale + c, count, hp->lr, trust_coefficient,
+                                                     hp->weight_decay); break;
+            case Q8_F16: e = q8::launch_layerwise_g1(kind, P, ctx, partial, scale + c, count, hp->lr, trust_coefficient,
+                                                     hp->weight_decay); break;
+            case Q8_BF16: e = q8::launch_layerwise_g2(kind, P, ctx, partial, scale + c, count, hp->lr, trust_coefficient,
+                                                      hp->weight_decay); break;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "layer-wise step launch");
+    }
+    return ok();
+}
+
 }  // namespace
 
 extern "C" {
@@ -669,44 +713,14 @@ q8_status q8_optim8bit_step_layerwise(q8_kind kind, q8_dtype g_dtype, const q8_t
     DeviceState* d = nullptr;
     if (q8_status s = device_state(&d); s != Q8_OK) return s;
     uint8_t* const ws = static_cast<uint8_t*>(workspace_dev);
-    unsigned int* count = reinterpret_cast<unsigned int*>(ws);
-    float* scale = reinterpret_cast<float*>(ws + Q8_LAYERWISE_SCALE_OFFSET);
-    double2* partial = reinterpret_cast<double2*>(ws + Q8_LAYERWISE_SCALE_OFFSET + lw_scale_bytes(num_tensors));
-    static thread_local q8::StepParams<kLwChunk> P;
-    P.s = make_scalars(hp, step, kind);
-    P.lw.lr = hp->lr;
-    P.lw.eta = trust_coefficient;
-    P.lw.wd = hp->weight_decay;
-    P.lw.gbar = reinterpret_cast<unsigned int*>(ws + kLwCountBytes);
     const q8::LaunchCtx ctx{d->tabs, d->sms, static_cast<cudaStream_t>(stream), q8::SEARCH_BUCKET, 0, 0};
-    for (int32_t c = 0; c < num_tensors; c += kLwChunk) {
-        // every tensor of the chunk keeps its slot (empty ones have no blocks) so that
-        // scale[i] belongs to tensors_host[i]
-        const int k = std::min(num_tensors - c, kLwChunk);
-        int64_t blocks = 0;
-        for (int j = 0; j < k; ++j) {
-            const q8_tensor& t = tensors_host[c + j];
-            P.t[j] = q8::TensorDesc{t.p, t.g, t.s1, t.s2, t.absmax1, t.absmax2, t.n};
-            P.block_start[j] = blocks;
-            blocks += (t.n + q8::kBlock - 1) / q8::kBlock;
-        }
-        P.num_tensors = k;
-        P.block_start[k] = blocks;
-        P.total_blocks = blocks;
-        P.scale = scale + c;
-        P.partial = partial;
-        cudaError_t e = cudaErrorInvalidValue;
-        switch (g_dtype) {
-            case Q8_F32: e = q8::launch_layerwise_g0(kind, P, ctx, partial, scale + c, count, hp->lr, trust_coefficient,
-                                                     hp->weight_decay); break;
-            case Q8_F16: e = q8::launch_layerwise_g1(kind, P, ctx, partial, scale + c, count, hp->lr, trust_coefficient,
-                                                     hp->weight_decay); break;
-            case Q8_BF16: e = q8::launch_layerwise_g2(kind, P, ctx, partial, scale + c, count, hp->lr, trust_coefficient,
-                                                      hp->weight_decay); break;
-        }
-        if (e != cudaSuccess) return cuda_fail(e, "layer-wise step launch");
+    // lists of <= kSmallMaxT tensors: the half-size descriptor table (fewer parameter bytes per launch)
+    if (num_tensors <= q8::kSmallMaxT) {
+        static thread_local q8::StepParams<q8::kSmallMaxT> Ps;
+        return layerwise_chunks(Ps, kind, g_dtype, tensors_host, num_tensors, hp, trust_coefficient, step, ws, ctx);
     }
-    return ok();
+    static thread_local q8::StepParams<kLwChunk> P;
+    return layerwise_chunks(P, kind, g_dtype, tensors_host, num_tensors, hp, trust_coefficient, step, ws, ctx);
 }
 
 }  // extern "C"

@@ -19,6 +19,9 @@ struct LaunchCtx {
 };
 
 constexpr int kMultiMaxT = 384;
+// Layer-wise lists of at most kSmallMaxT tensors launch with a half-size descriptor table: the kernel
+// parameters are copied at every launch (~0.05 us per KB, DESIGN 12b), and a LARS step is two launches.
+constexpr int kSmallMaxT = 192;
 
 // Launch the fused step for gradient dtype g<N> (0 fp32, 1 fp16, 2 bf16); exactly one of
 // single / multi is non-NULL.  Returns the launch error (cudaSuccess if ok).
@@ -37,6 +40,12 @@ cudaError_t launch_layerwise_g0(int kind, const StepParams<kMultiMaxT>& P, const
 cudaError_t launch_layerwise_g1(int kind, const StepParams<kMultiMaxT>& P, const LaunchCtx& ctx, double2* partial,
                                 float* scale, unsigned int* count, double lr, double eta, double wd);
 cudaError_t launch_layerwise_g2(int kind, const StepParams<kMultiMaxT>& P, const LaunchCtx& ctx, double2* partial,
+                                float* scale, unsigned int* count, double lr, double eta, double wd);
+cudaError_t launch_layerwise_g0(int kind, const StepParams<kSmallMaxT>& P, const LaunchCtx& ctx, double2* partial,
+                                float* scale, unsigned int* count, double lr, double eta, double wd);
+cudaError_t launch_layerwise_g1(int kind, const StepParams<kSmallMaxT>& P, const LaunchCtx& ctx, double2* partial,
+                                float* scale, unsigned int* count, double lr, double eta, double wd);
+cudaError_t launch_layerwise_g2(int kind, const StepParams<kSmallMaxT>& P, const LaunchCtx& ctx, double2* partial,
                                 float* scale, unsigned int* count, double lr, double eta, double wd);
 
 // Fused ZeRO-1 step (MODE_ZERO) for gradient dtype g<N> with exactly `grid` CTAs (identical on

@@ -104,14 +104,14 @@ cudaError_t launch_any(int kind, const StepParams<MAXT>& P, const LaunchCtx& ctx
 }
 
 // Layer-wise kinds (LAMB, LARS): norms -> per-tensor scale -> fused step, default configuration.
-template <int KIND>
-cudaError_t launch_layerwise_t(const StepParams<kMultiMaxT>& P, const LaunchCtx& ctx, double2* partial,
+template <int KIND, int MAXT>
+cudaError_t launch_layerwise_t(const StepParams<MAXT>& P, const LaunchCtx& ctx, double2* partial,
                                float* scale, unsigned int* count, double lr, double eta, double wd) {
     constexpr int G = Q8_GDT;
     constexpr int NS = G == G_F32 ? 3 : 4;
     constexpr int SUBT = G == G_F32 ? 256 : 128;
     if (P.total_blocks == 0) {  // only empty tensors: their scale is still defined (lr)
-        layer_scale_kernel<KIND, kMultiMaxT><<<P.num_tensors, kScaleThreads, 0, ctx.stream>>>(P, partial, scale, lr, eta, wd,
+        layer_scale_kernel<KIND, MAXT><<<P.num_tensors, kScaleThreads, 0, ctx.stream>>>(P, partial, scale, lr, eta, wd,
                                                                                         0);
         return cudaGetLastError();
     }
@@ -125,7 +125,7 @@ cudaError_t launch_layerwise_t(const StepParams<kMultiMaxT>& P, const LaunchCtx&
         return v && std::atoi(v) == 1;
     }();
     if constexpr (KIND == KIND_LARS) if (one_launch) {
-        const auto fn = optim8bit_step_kernel<KIND, G, kMultiMaxT, SEARCH_BUCKET, NS, SUBT, MODE_LARSF>;
+        const auto fn = optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, NS, SUBT, MODE_LARSF>;
         const int smem = step_smem_bytes(NS, G);
         e = ensure_smem(reinterpret_cast<const void*>(fn), smem);
         if (e != cudaSuccess) return e;
@@ -146,33 +146,33 @@ cudaError_t launch_layerwise_t(const StepParams<kMultiMaxT>& P, const LaunchCtx&
         return cudaLaunchKernelEx(&cfg, fn, P, ctx.tabs);
     }
     if constexpr (KIND == KIND_LAMB) {
-        e = persistent(optim8bit_step_kernel<KIND, G, kMultiMaxT, SEARCH_BUCKET, NS, SUBT, MODE_NORMS>, NS, SUBT,
+        e = persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, NS, SUBT, MODE_NORMS>, NS, SUBT,
                        P.total_blocks, ctx, P, ctx.tabs);
     } else {
         static int occ = [] {
             int o = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, lars_norms_kernel<G, kMultiMaxT>, kThreads, 0) !=
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, lars_norms_kernel<G, MAXT>, kThreads, 0) !=
                     cudaSuccess || o < 1)
                 o = 1;
             return o;
         }();
         // norms + per-tensor scales in one pass, then the step as a dependent launch (q8_layerwise.cuh)
         const int64_t g1 = std::min<int64_t>(P.total_blocks, static_cast<int64_t>(ctx.sms) * occ);
-        lars_norms_kernel<G, kMultiMaxT><<<static_cast<unsigned>(g1), kThreads, 0, ctx.stream>>>(P, count, scale);
+        lars_norms_kernel<G, MAXT><<<static_cast<unsigned>(g1), kThreads, 0, ctx.stream>>>(P, count, scale);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        return persistent_pdl(optim8bit_step_kernel<KIND, G, kMultiMaxT, SEARCH_BUCKET, NS, SUBT>, NS, SUBT,
+        return persistent_pdl(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, NS, SUBT>, NS, SUBT,
                               P.total_blocks, ctx, P, ctx.tabs);
     }
     if (e != cudaSuccess) return e;
     // LAMB (the only kind that gets here): the norms pass wrote one partial per warp per tensor segment of
     // each of its grid * NS sub-blocks, in the slot of the segment's last block
     const int64_t nsubs = persistent_grid(P.total_blocks, NS, ctx.sms) * NS;
-    lamb_scale_kernel<kMultiMaxT><<<P.num_tensors, kScaleThreads, 0, ctx.stream>>>(P, partial, scale, lr, SUBT / 32,
+    lamb_scale_kernel<MAXT><<<P.num_tensors, kScaleThreads, 0, ctx.stream>>>(P, partial, scale, lr, SUBT / 32,
                                                                                   nsubs);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    return persistent(optim8bit_step_kernel<KIND, G, kMultiMaxT, SEARCH_BUCKET, NS, SUBT>, NS, SUBT, P.total_blocks,
+    return persistent(optim8bit_step_kernel<KIND, G, MAXT, SEARCH_BUCKET, NS, SUBT>, NS, SUBT, P.total_blocks,
                       ctx, P, ctx.tabs);
 }
 
@@ -191,8 +191,15 @@ namespace q8 {
 cudaError_t Q8_CAT(launch_layerwise_g, Q8_GDT)(int kind, const StepParams<kMultiMaxT>& P, const LaunchCtx& ctx,
                                                double2* partial, float* scale, unsigned int* count, double lr,
                                                double eta, double wd) {
-    if (kind == KIND_LAMB) return launch_layerwise_t<KIND_LAMB>(P, ctx, partial, scale, count, lr, eta, wd);
-    if (kind == KIND_LARS) return launch_layerwise_t<KIND_LARS>(P, ctx, partial, scale, count, lr, eta, wd);
+    if (kind == KIND_LAMB) return launch_layerwise_t<KIND_LAMB, kMultiMaxT>(P, ctx, partial, scale, count, lr, eta, wd);
+    if (kind == KIND_LARS) return launch_layerwise_t<KIND_LARS, kMultiMaxT>(P, ctx, partial, scale, count, lr, eta, wd);
+    return cudaErrorInvalidValue;
+}
+cudaError_t Q8_CAT(launch_layerwise_g, Q8_GDT)(int kind, const StepParams<kSmallMaxT>& P, const LaunchCtx& ctx,
+                                               double2* partial, float* scale, unsigned int* count, double lr,
+                                               double eta, double wd) {
+    if (kind == KIND_LAMB) return launch_layerwise_t<KIND_LAMB, kSmallMaxT>(P, ctx, partial, scale, count, lr, eta, wd);
+    if (kind == KIND_LARS) return launch_layerwise_t<KIND_LARS, kSmallMaxT>(P, ctx, partial, scale, count, lr, eta, wd);
     return cudaErrorInvalidValue;
 }
 }  // namespace q8

@@ -140,6 +140,20 @@ def test_layerwise_chunks_over_384_tensors(q8, kind):
     _assert_equal(kind, ents, refs)
 
 
+@pytest.mark.parametrize("count", [192, 193])
+def test_layerwise_descriptor_table_tiers(q8, count):
+    """Lists of <= 192 tensors launch with the 192-entry descriptor table, longer ones with the 384-entry
+    table (q8_launch.h kSmallMaxT): both sides of the boundary, LAMB and LARS, bit for bit (teacher-forced)."""
+    rng = np.random.default_rng(count)
+    sizes = [int(x) for x in rng.integers(1, 5000, size=count)]
+    for kind in ("lars", "lamb"):
+        ents, refs = _make(kind, sizes, "float16", seed0=count)
+        got, exp = _step_both(q8, kind, ents, refs, sizes, "float16", 2, HP[kind], teacher_force=True)
+        ulps = np.abs(got.view(np.int32).astype(np.int64) - exp.view(np.int32).astype(np.int64))
+        assert ulps.max() <= 1, (got, exp)
+        _assert_equal(kind, ents, refs)
+
+
 def test_lars_resnet50_layer_list(q8):
     """LARS's home workload: the 161 ResNet-50 tensors, bf16 grads, 2 steps."""
     sizes = [int(np.prod(s)) for s in synth.resnet50_shapes()]
