@@ -215,6 +215,20 @@ q8_status dispatch_step(q8_kind kind, q8_dtype gdt, const q8::StepParams<MAXT>& 
     return Q8_OK;
 }
 
+// Plans of <= kSmallMaxT non-empty tensors: one launch with the 192-entry descriptor table.
+q8_status dispatch_plan_small(q8_kind kind, q8_dtype gdt, const q8::StepParams<q8::kSmallMaxT>& P,
+                              const DeviceState* d, cudaStream_t st) {
+    const q8::LaunchCtx ctx{d->tabs, d->sms, st, q8::SEARCH_BUCKET, 0, 0, 1};
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (gdt) {
+        case Q8_F32: e = q8::launch_plan_small_g0(kind, P, ctx); break;
+        case Q8_F16: e = q8::launch_plan_small_g1(kind, P, ctx); break;
+        case Q8_BF16: e = q8::launch_plan_small_g2(kind, P, ctx); break;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "optim8bit_step_kernel launch");
+    return Q8_OK;
+}
+
 q8_status check_common(q8_dtype gdt, int32_t blocksize) {
     if (gdt != Q8_F32 && gdt != Q8_F16 && gdt != Q8_BF16) return fail(Q8_ERR_INVALID, "bad g_dtype %d", gdt);
     if (blocksize != q8::kBlock)
@@ -817,6 +831,8 @@ struct q8_plan {
     q8_dtype gdt = Q8_F32;
     int32_t count = 0;
     std::vector<std::unique_ptr<q8::StepParams<q8::kMultiMaxT>>> chunks;
+    // plans of <= kSmallMaxT non-empty tensors: their one launch with the 192-entry table (chunks empty)
+    std::unique_ptr<q8::StepParams<q8::kSmallMaxT>> small;
     std::vector<int32_t> chunk_of, slot_of;  // per plan tensor; -1 for empty tensors
     unsigned int* done = nullptr;             // CTA completion counter of capturable launches
 };
@@ -901,6 +917,18 @@ q8_status q8_plan_create(q8_kind kind, q8_dtype g_dtype, const q8_tensor* t8, in
         plan->chunk_of[k] = static_cast<int32_t>(plan->chunks.size() - 1);
         plan->slot_of[k] = slot;
     }
+    if (plan->chunks.size() == 1 && plan->chunks[0]->num_tensors <= q8::kSmallMaxT) {
+        const q8::StepParams<MAXT>& B = *plan->chunks[0];
+        plan->small = std::make_unique<q8::StepParams<q8::kSmallMaxT>>();
+        q8::StepParams<q8::kSmallMaxT>& S = *plan->small;
+        S.scale = B.scale;
+        S.partial = B.partial;
+        S.num_tensors = B.num_tensors;
+        S.total_blocks = B.total_blocks;
+        for (int j = 0; j <= B.num_tensors; ++j) S.block_start[j] = B.block_start[j];
+        for (int j = 0; j < B.num_tensors; ++j) S.t[j] = B.t[j];
+        plan->chunks.clear();  // chunk_of stays 0: the slot indices are the small table's
+    }
     e = cudaMalloc(&plan->done, sizeof(unsigned int));
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(plan counter)");
     e = cudaMemset(plan->done, 0, sizeof(unsigned int));
@@ -919,7 +947,10 @@ q8_status q8_plan_set_grads(q8_plan* plan, const void* const* g_host, int32_t co
         const void* g = g_host[k];
         if (!g || plan->chunk_of[k] < 0) continue;
         if (!aligned(g, 16)) return fail(Q8_ERR_INVALID, "tensor %d: g not 16-byte aligned", k);
-        plan->chunks[plan->chunk_of[k]]->t[plan->slot_of[k]].g = g;
+        if (plan->small)
+            plan->small->t[plan->slot_of[k]].g = g;
+        else
+            plan->chunks[plan->chunk_of[k]]->t[plan->slot_of[k]].g = g;
     }
     return ok();
 }
@@ -931,6 +962,12 @@ q8_status q8_plan_step(q8_plan* plan, const q8_hparams* hp, int64_t step, void* 
     DeviceState* d = nullptr;
     if (q8_status s = device_state(&d); s != Q8_OK) return s;
     const q8::StepScalars sc = make_scalars(hp, step);
+    if (plan->small) {
+        plan->small->s = sc;
+        plan->small->ds.step = nullptr;
+        const q8_status s = dispatch_plan_small(plan->kind, plan->gdt, *plan->small, d, static_cast<cudaStream_t>(stream));
+        return s == Q8_OK ? ok() : s;
+    }
     for (auto& P : plan->chunks) {
         P->s = sc;
         P->ds.step = nullptr;
@@ -949,20 +986,29 @@ q8_status q8_plan_step_device(q8_plan* plan, const q8_hparams* hp, int64_t* step
     if (q8_status s = plan_device_check(plan); s != Q8_OK) return s;
     DeviceState* d = nullptr;
     if (q8_status s = device_state(&d); s != Q8_OK) return s;
+    auto arm = [&](auto& P, bool last) {
+        P.s = make_scalars(hp, 1);  // placeholder; the kernel uses ds (its wd decides the L2 variant)
+        P.ds.step = step_dev;
+        P.ds.done = plan->done;
+        P.ds.advance = last ? 1 : 0;
+        P.ds.kind = plan->kind;
+        P.ds.lr = hp->lr;
+        P.ds.beta1 = hp->beta1;
+        P.ds.beta2 = hp->beta2;
+        P.ds.eps = hp->eps;
+        P.ds.wd = hp->weight_decay;
+        P.ds.bias_correction = hp->bias_correction;
+    };
+    if (plan->small) {
+        arm(*plan->small, true);
+        q8_status s = dispatch_plan_small(plan->kind, plan->gdt, *plan->small, d, static_cast<cudaStream_t>(stream));
+        plan->small->ds.step = nullptr;
+        return s == Q8_OK ? ok() : s;
+    }
     const size_t nc = plan->chunks.size();
     for (size_t c = 0; c < nc; ++c) {
         auto& P = plan->chunks[c];
-        P->s = make_scalars(hp, 1);  // placeholder; the kernel uses ds (its wd decides the L2 variant)
-        P->ds.step = step_dev;
-        P->ds.done = plan->done;
-        P->ds.advance = c + 1 == nc ? 1 : 0;
-        P->ds.kind = plan->kind;
-        P->ds.lr = hp->lr;
-        P->ds.beta1 = hp->beta1;
-        P->ds.beta2 = hp->beta2;
-        P->ds.eps = hp->eps;
-        P->ds.wd = hp->weight_decay;
-        P->ds.bias_correction = hp->bias_correction;
+        arm(*P, c + 1 == nc);
         q8_status s =
             dispatch_step<q8::kMultiMaxT>(plan->kind, plan->gdt, *P, d, static_cast<cudaStream_t>(stream), 1);
         P->ds.step = nullptr;

@@ -32,6 +32,12 @@ cudaError_t launch_step_g1(int kind, const StepParams<1>* single, const StepPara
 cudaError_t launch_step_g2(int kind, const StepParams<1>* single, const StepParams<kMultiMaxT>* multi,
                            const LaunchCtx& ctx);
 
+// Plan launch (the PLAN instantiation of the fused step) with the 192-entry descriptor table, for plans of
+// <= kSmallMaxT non-empty tensors.
+cudaError_t launch_plan_small_g0(int kind, const StepParams<kSmallMaxT>& P, const LaunchCtx& ctx);
+cudaError_t launch_plan_small_g1(int kind, const StepParams<kSmallMaxT>& P, const LaunchCtx& ctx);
+cudaError_t launch_plan_small_g2(int kind, const StepParams<kSmallMaxT>& P, const LaunchCtx& ctx);
+
 // Layer-wise step (LAMB / LARS) for gradient dtype g<N>: norms pass, per-tensor scale pass
 // (writes scale[0 .. P.num_tensors)), fused step; partial holds P.total_blocks entries; count holds
 // P.num_tensors block counters, zero on entry and on return (LARS: the scales come from its norms pass).

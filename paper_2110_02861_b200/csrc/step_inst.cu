@@ -180,6 +180,29 @@ cudaError_t launch_layerwise_t(const StepParams<MAXT>& P, const LaunchCtx& ctx, 
 
 #define Q8_CAT2(a, b) a##b
 #define Q8_CAT(a, b) Q8_CAT2(a, b)
+namespace {
+template <int KIND>
+cudaError_t launch_plan_small_kind(const StepParams<kSmallMaxT>& P, const LaunchCtx& ctx) {
+    constexpr int G = Q8_GDT;
+    constexpr int NS = G == G_F32 ? 3 : 4;
+    constexpr int SUBT = G == G_F32 ? 256 : 128;
+    return persistent(optim8bit_step_kernel<KIND, G, kSmallMaxT, SEARCH_BUCKET, NS, SUBT, MODE_STEP, true>, NS, SUBT,
+                      P.total_blocks, ctx, P, ctx.tabs);
+}
+}  // namespace
+
+cudaError_t Q8_CAT(launch_plan_small_g, Q8_GDT)(int kind, const StepParams<kSmallMaxT>& P, const LaunchCtx& ctx) {
+    switch (kind) {
+        case KIND_ADAM:
+            return P.s.wd != 0.0f ? launch_plan_small_kind<KIND_ADAM | KIND_L2>(P, ctx) : launch_plan_small_kind<KIND_ADAM>(P, ctx);
+        case KIND_ADAMW: return launch_plan_small_kind<KIND_ADAMW>(P, ctx);
+        case KIND_MOMENTUM:
+            return P.s.wd != 0.0f ? launch_plan_small_kind<KIND_MOMENTUM | KIND_L2>(P, ctx)
+                                  : launch_plan_small_kind<KIND_MOMENTUM>(P, ctx);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 cudaError_t Q8_CAT(launch_step_g, Q8_GDT)(int kind, const StepParams<1>* single,
                                           const StepParams<kMultiMaxT>* multi, const LaunchCtx& ctx) {
     return single ? launch_any<1>(kind, *single, ctx) : launch_any<kMultiMaxT>(kind, *multi, ctx);

@@ -68,15 +68,17 @@ def _assert_same(kind, e8, e32, ref8, ref32):
             assert np.array_equal(e[3].cpu().numpy().view(np.uint32), r[2].view(np.uint32)), f"r {i}"
 
 
+@pytest.mark.parametrize("count", [450, 192])
 @pytest.mark.parametrize("kind,gdt,device_step", [("adamw", "bfloat16", False), ("adam", "float16", True),
                                                   ("momentum", "float32", False), ("adamw", "float32", True),
                                                   ("momentum", "bfloat16", True)])
-def test_mixed_plan_matches_oracle(q8, kind, gdt, device_step):
-    """450 tensors (two launches of <= 384), every third one with 32-bit states, 3 steps."""
+def test_mixed_plan_matches_oracle(q8, kind, gdt, device_step, count):
+    """450 tensors (two launches of <= 384) or 192 (one launch with the 192-entry descriptor table,
+    q8_launch.h kSmallMaxT), every third one with 32-bit states, 3 steps."""
     hp = dict(synth.HPARAMS[kind])
     if kind == "adam":
         hp["weight_decay"] = 1e-3      # L2 variant of the kernel
-    sizes = _sizes(11, 450)
+    sizes = _sizes(11, count)
     e8, e32, ref8, ref32 = _make(kind, gdt, sizes, 3, seed=3)
     step_t = torch.zeros(1, dtype=torch.int64, device=DEV)
     plan = None
